@@ -1,0 +1,41 @@
+// Host-side Q1 assembly into 9-diagonal coefficient arrays.
+//
+// Restates the reference's element formulas (fem.cpp:35-106: 2x2 Gauss mass,
+// stiffness and SUPG convection-diffusion elements) and its Dirichlet
+// elimination (fem.cpp:109-140), but assembles straight into the
+// structure-of-arrays 9-point layout the device kernels read (Op9) instead
+// of a triplet buffer + CSR. Entry d = (dy+1)*3+(dx+1) for node i holds
+// A(i, i + dx + dy*nx); neighbours outside the interior hold 0.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+namespace ocb {
+
+inline int level_nx(int level) { return (1 << level) - 1; }
+inline long long level_n(int level)
+{
+    const long long nx = level_nx(level);
+    return nx * nx;
+}
+
+enum class AssembleKind { mass = 0, poisson = 1, convdiff = 2, partial_mass = 3, lumped = 4 };
+
+std::vector<double> assemble_mass9(int level);
+std::vector<double> assemble_poisson9(int level);
+std::vector<double> assemble_convdiff9(int level, double eps, bool supg = true);
+std::vector<double> assemble_partial_mass9(int level, const double obs[4]);
+/// Row sums of the Dirichlet-eliminated consistent mass (qp.cpp:137).
+std::vector<double> lumped_diag(int level);
+/// Transpose of a 9-point operator: T(i, i+d) = A(i+d, i).
+std::vector<double> transpose9(const std::vector<double>& coef, int level);
+/// If every stored entry equals the interior stencil, return true and the
+/// 9 constants (the grid-constant operators L, M, M+tau L).
+bool constant_stencil(const std::vector<double>& coef, int level, double c[9]);
+/// Nodal interpolation of the default wind (fem.cpp:164-169) is inside
+/// assemble_convdiff9; this exposes the element-centre SUPG delta for tests.
+double supg_delta(int level, int ex, int ey, double eps);
+
+} // namespace ocb

@@ -1,0 +1,408 @@
+// extern "C" boundary (include/optcon_b200.h): catches the library's C++
+// exceptions and maps them to status codes mirroring the reference's
+// exception classes (invalid_argument -> 1, runtime_error -> 2).
+#include "assembly.hpp"
+#include "solver.hpp"
+
+#include <cstring>
+#include <string>
+
+struct oc_ctx {
+    ocb::Ctx ctx;
+    explicit oc_ctx(int dev) : ctx(dev) {}
+};
+
+struct oc_problem {
+    std::unique_ptr<ocb::Problem> p;
+};
+
+struct oc_mg {
+    ocb::Ctx* ctx = nullptr;
+    int level = 0;
+    ocb::DVec fine;
+    std::vector<ocb::DVec> base;
+    ocb::Hierarchy h;
+    ocb::DVec t0, t1;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f)
+{
+    try {
+        f();
+        return OC_OK;
+    } catch (const ocb::CudaFailure& e) {
+        g_err = e.what();
+        return OC_CUDA_ERROR;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return OC_INVALID_ARGUMENT;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return OC_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return OC_RUNTIME_ERROR;
+    }
+}
+
+void require(const void* p, const char* what)
+{
+    if (!p) throw ocb::InvalidArgument(std::string(what) + ": null argument");
+}
+
+} // namespace
+
+extern "C" {
+
+const char* oc_last_error(void) { return g_err.c_str(); }
+int oc_abi_version(void) { return OC_ABI_VERSION; }
+
+int oc_create(oc_ctx** out, int device)
+{
+    return guarded([&] {
+        require(out, "oc_create");
+        *out = new oc_ctx(device);
+    });
+}
+
+void oc_destroy(oc_ctx* c) { delete c; }
+
+int oc_synchronize(oc_ctx* c)
+{
+    return guarded([&] {
+        require(c, "oc_synchronize");
+        c->ctx.sync();
+    });
+}
+
+int oc_problem_create(oc_ctx* c, const oc_problem_desc* d, oc_problem** out)
+{
+    return guarded([&] {
+        require(c, "oc_problem_create");
+        require(d, "oc_problem_create");
+        require(out, "oc_problem_create");
+        auto p = std::make_unique<oc_problem>();
+        p->p = std::make_unique<ocb::Problem>(c->ctx, *d);
+        *out = p.release();
+    });
+}
+
+void oc_problem_destroy(oc_problem* p) { delete p; }
+
+int oc_problem_info_get(oc_problem* p, oc_problem_info* info)
+{
+    return guarded([&] {
+        require(p, "oc_problem_info_get");
+        require(info, "oc_problem_info_get");
+        *info = p->p->info();
+    });
+}
+
+int oc_default_params(oc_ipm_params* p)
+{
+    return guarded([&] {
+        require(p, "oc_default_params");
+        // IpmParams defaults (ipm.hpp:17-32)
+        p->alpha0 = 0.995;
+        p->sigma = 0.2;
+        p->eps_p = p->eps_d = p->eps_c = 1e-6;
+        p->mu0 = 1.0;
+        p->max_iterations = 100;
+        p->linear_tol = 1e-10;
+        p->linear_maxit = 200;
+        p->cheb_steps = 20;
+        p->mg_cycles = 3;
+        p->mg_pre = 5;
+        p->mg_post = 5;
+        p->solver = OC_SOLVER_GMRES_PT;
+        p->smoother = OC_SMOOTHER_COLOR4;
+        p->gmres_restart = 0;
+    });
+}
+
+int oc_ipm_solve(oc_problem* p, const oc_ipm_params* params, oc_ipm_result* r)
+{
+    return guarded([&] {
+        require(p, "oc_ipm_solve");
+        require(params, "oc_ipm_solve");
+        require(r, "oc_ipm_solve");
+        p->p->ipm_solve(*params, r);
+    });
+}
+
+int oc_kkt_apply(oc_problem* p, const double* ty, const double* tw, const double* tv,
+                 const double* x, double* out)
+{
+    return guarded([&] {
+        require(p, "oc_kkt_apply");
+        require(tw, "oc_kkt_apply");
+        require(tv, "oc_kkt_apply");
+        require(x, "oc_kkt_apply");
+        require(out, "oc_kkt_apply");
+        ocb::Problem& P = *p->p;
+        const size_t n4 = 4 * (size_t)P.P.ny;
+        P.set_theta(ty, tw, tv);
+        ocb::DVec xin(n4), o(n4);
+        ocb::copy_any(P.ctx, xin.get(), x, n4 * 8);
+        P.kkt(xin.get(), o.get());
+        ocb::copy_any(P.ctx, out, o.get(), n4 * 8);
+        P.ctx.sync();
+    });
+}
+
+int oc_precond_setup(oc_problem* p, const double* ty, const double* tw, const double* tv,
+                     const oc_ipm_params* params)
+{
+    return guarded([&] {
+        require(p, "oc_precond_setup");
+        require(params, "oc_precond_setup");
+        ocb::Problem& P = *p->p;
+        P.set_theta(ty, tw, tv);
+        const oc_problem_info info = P.info();
+        int kind = params->solver == OC_SOLVER_GMRES_PPI ? OC_PRECOND_PPI
+                   : params->solver == OC_SOLVER_MINRES_PD ? OC_PRECOND_PD
+                                                           : OC_PRECOND_PT;
+        if (info.partial_observation && kind != OC_PRECOND_PPI)
+            throw ocb::InvalidArgument(kind == OC_PRECOND_PD
+                                           ? "minres-pd requires a nonsingular (1,1) block"
+                                           : "gmres-pt requires a nonsingular (1,1) block");
+        P.setup_precond(kind, *params);
+        P.ctx.sync();
+    });
+}
+
+int oc_precond_apply(oc_problem* p, int kind, const double* r, double* out)
+{
+    return guarded([&] {
+        require(p, "oc_precond_apply");
+        require(r, "oc_precond_apply");
+        require(out, "oc_precond_apply");
+        ocb::Problem& P = *p->p;
+        const size_t n4 = 4 * (size_t)P.P.ny;
+        ocb::DVec rin(n4), o(n4);
+        ocb::copy_any(P.ctx, rin.get(), r, n4 * 8);
+        P.precond_apply(kind, rin.get(), o.get());
+        ocb::copy_any(P.ctx, out, o.get(), n4 * 8);
+        P.ctx.sync();
+    });
+}
+
+int oc_schur_apply(oc_problem* p, const double* r, double* out)
+{
+    return guarded([&] {
+        require(p, "oc_schur_apply");
+        ocb::Problem& P = *p->p;
+        const size_t n = (size_t)P.P.ny;
+        ocb::DVec rin(n), o(n);
+        ocb::copy_any(P.ctx, rin.get(), r, n * 8);
+        P.schur_apply(rin.get(), o.get());
+        ocb::copy_any(P.ctx, out, o.get(), n * 8);
+        P.ctx.sync();
+    });
+}
+
+int oc_newton_solve(oc_problem* p, const double* ty, const double* tw, const double* tv,
+                    const double* r1, const double* r2, const double* r3,
+                    const oc_ipm_params* params, double* dy, double* dz, double* dp,
+                    oc_solve_report* report)
+{
+    return guarded([&] {
+        require(p, "oc_newton_solve");
+        require(params, "oc_newton_solve");
+        ocb::Problem& P = *p->p;
+        const size_t n = (size_t)P.P.ny;
+        P.set_theta(ty, tw, tv);
+        ocb::DVec rhs(4 * n), x(4 * n);
+        ocb::copy_any(P.ctx, rhs.get(), r1, n * 8);
+        ocb::copy_any(P.ctx, rhs.get() + n, r2, 2 * n * 8);
+        ocb::copy_any(P.ctx, rhs.get() + 3 * n, r3, n * 8);
+        const oc_solve_report rep = P.newton_solve(*params, rhs.get(), x.get());
+        if (dy) ocb::copy_any(P.ctx, dy, x.get(), n * 8);
+        if (dz) ocb::copy_any(P.ctx, dz, x.get() + n, 2 * n * 8);
+        if (dp) ocb::copy_any(P.ctx, dp, x.get() + 3 * n, n * 8);
+        P.ctx.sync();
+        if (report) *report = rep;
+    });
+}
+
+int oc_ipm_pieces(oc_problem* p, const double* y, const double* z, const double* pv,
+                  const double* lya, const double* lyb, const double* lza, const double* lzb,
+                  double mu_state, double mu_rhs, double* ty, double* tw, double* tv, double* r1,
+                  double* r2, double* r3, double* norms3)
+{
+    return guarded([&] {
+        require(p, "oc_ipm_pieces");
+        p->p->ipm_pieces(y, z, pv, lya, lyb, lza, lzb, mu_state, mu_rhs, ty, tw, tv, r1, r2, r3,
+                         norms3);
+    });
+}
+
+int oc_objective(oc_problem* p, const double* y, const double* z, double* out)
+{
+    return guarded([&] {
+        require(p, "oc_objective");
+        require(out, "oc_objective");
+        *out = p->p->objective(y, z);
+    });
+}
+
+int oc_time_applies(oc_problem* p, int kind, int reps, double* kkt_ms, double* prec_ms)
+{
+    return guarded([&] {
+        require(p, "oc_time_applies");
+        if (reps < 1) throw ocb::InvalidArgument("oc_time_applies: reps must be >= 1");
+        p->p->time_applies(kind, reps, kkt_ms, prec_ms);
+    });
+}
+
+int oc_mg_create(oc_ctx* c, int level, const double* coef9, int rediscretize, double eps,
+                 oc_mg** out)
+{
+    return guarded([&] {
+        require(c, "oc_mg_create");
+        require(coef9, "oc_mg_create");
+        require(out, "oc_mg_create");
+        if (level < 3) throw ocb::InvalidArgument("MgHierarchy: fine level must be >= 3");
+        auto m = std::make_unique<oc_mg>();
+        m->ctx = &c->ctx;
+        m->level = level;
+        const long long n = ocb::level_n(level);
+        m->fine.resize(9 * (size_t)n);
+        ocb::copy_any(c->ctx, m->fine.get(), coef9, 9 * (size_t)n * 8);
+        m->h.allocate(level);
+        ocb::Op9 f{};
+        f.nx = ocb::level_nx(level);
+        f.coef = m->fine.get();
+        f.cscale = 1.0;
+        if (rediscretize) {
+            std::vector<const double*> b;
+            for (int l = level; l >= 2; --l) {
+                std::vector<double> a = ocb::assemble_convdiff9(l, eps, true);
+                if (rediscretize == 2) a = ocb::transpose9(a, l);
+                m->base.emplace_back(a.size());
+                ocb::copy_any(c->ctx, m->base.back().get(), a.data(), a.size() * 8);
+                c->ctx.sync();
+            }
+            for (auto& v : m->base) b.push_back(v.get());
+            m->h.build_rediscretized(c->ctx, f, b);
+        } else {
+            m->h.build(c->ctx, f);
+        }
+        m->t0.resize((size_t)n);
+        m->t1.resize((size_t)n);
+        c->ctx.sync();
+        *out = m.release();
+    });
+}
+
+int oc_mg_solve(oc_mg* m, const double* rhs, int cycles, int pre, int post, double* out)
+{
+    return guarded([&] {
+        require(m, "oc_mg_solve");
+        const long long n = ocb::level_n(m->level);
+        ocb::copy_any(*m->ctx, m->t0.get(), rhs, (size_t)n * 8);
+        ocb::DevArray<int> flags(1);
+        cudaMemsetAsync(flags.get(), 0, sizeof(int), m->ctx->stream);
+        ocb::MgParams p;
+        p.cycles = cycles;
+        p.pre = pre;
+        p.post = post;
+        m->h.solve(*m->ctx, m->t0.get(), m->t1.get(), p, 0, flags.get());
+        ocb::copy_any(*m->ctx, out, m->t1.get(), (size_t)n * 8);
+        cudaMemcpyAsync(m->ctx->hflags, flags.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                        m->ctx->stream);
+        m->ctx->sync();
+        if (m->ctx->hflags[0] & ocb::kErrMgDiverged)
+            throw ocb::RuntimeError("MgHierarchy::solve: residual growth, cycle diverged");
+    });
+}
+
+int oc_mg_depth(oc_mg* m) { return m ? m->h.depth() : -1; }
+
+int oc_mg_level_matrix(oc_mg* m, int k, double* coef9)
+{
+    return guarded([&] {
+        require(m, "oc_mg_level_matrix");
+        if (k < 0 || k > m->h.depth()) throw ocb::InvalidArgument("oc_mg_level_matrix: bad level");
+        const ocb::Op9 a = m->h.level_op(k, 0);
+        ocb::copy_any(*m->ctx, coef9, a.coef, 9 * (size_t)m->h.level_n(k) * 8);
+        m->ctx->sync();
+    });
+}
+
+int oc_mg_smooth(oc_mg* m, const double* b, double* x, int forward)
+{
+    return guarded([&] {
+        require(m, "oc_mg_smooth");
+        const long long n = ocb::level_n(m->level);
+        ocb::copy_any(*m->ctx, m->t0.get(), b, (size_t)n * 8);
+        ocb::copy_any(*m->ctx, m->t1.get(), x, (size_t)n * 8);
+        m->h.smooth(*m->ctx, m->t0.get(), m->t1.get(), forward != 0, 0);
+        ocb::copy_any(*m->ctx, x, m->t1.get(), (size_t)n * 8);
+        m->ctx->sync();
+    });
+}
+
+void oc_mg_destroy(oc_mg* m) { delete m; }
+
+int oc_cheb_apply(oc_ctx* c, int level, double scale, const double* extra, int steps,
+                  const double* b, double* x)
+{
+    return guarded([&] {
+        require(c, "oc_cheb_apply");
+        if (steps < 1) throw ocb::InvalidArgument("chebyshev: steps must be >= 1");
+        ocb::Ctx& cx = c->ctx;
+        const int nx = ocb::level_nx(level);
+        const long long n = (long long)nx * nx;
+        const std::vector<double> M9 = ocb::assemble_mass9(level);
+        ocb::ProbDev P{};
+        P.nx = nx;
+        P.ns = n;
+        P.nt = 1;
+        P.ny = n;
+        P.heat = 1; // scale applied as the per-block weight tau*w_0 = scale
+        P.tau = scale;
+        P.M.nx = nx;
+        P.M.cscale = 1.0;
+        for (int d = 0; d < 9; ++d) P.M.c[d] = M9[d * n + n / 2];
+        const double one = 1.0;
+        ocb::DVec qw(1), bb((size_t)n), e, out((size_t)n), g((size_t)n), r0((size_t)n),
+            r1((size_t)n), r2((size_t)n);
+        ocb::copy_any(cx, qw.get(), &one, 8);
+        P.qw = qw.get();
+        ocb::copy_any(cx, bb.get(), b, (size_t)n * 8);
+        if (extra) {
+            e.resize((size_t)n);
+            ocb::copy_any(cx, e.get(), extra, (size_t)n * 8);
+        }
+        ocb::ChebWork w{g.get(), r0.get(), r1.get(), r2.get()};
+        ocb::launch_chebyshev(cx.stream, P, bb.get(), extra ? e.get() : nullptr, steps, w,
+                              out.get());
+        ocb::copy_any(cx, x, out.get(), (size_t)n * 8);
+        cx.sync();
+    });
+}
+
+int oc_assemble9(int what, int level, double eps, const double* obs, double* coef)
+{
+    return guarded([&] {
+        require(coef, "oc_assemble9");
+        std::vector<double> a;
+        switch (what) {
+        case 0: a = ocb::assemble_mass9(level); break;
+        case 1: a = ocb::assemble_poisson9(level); break;
+        case 2: a = ocb::assemble_convdiff9(level, eps, true); break;
+        case 3: require(obs, "oc_assemble9"); a = ocb::assemble_partial_mass9(level, obs); break;
+        case 4: a = ocb::lumped_diag(level); break;
+        default: throw ocb::InvalidArgument("oc_assemble9: unknown operator");
+        }
+        std::memcpy(coef, a.data(), a.size() * sizeof(double));
+    });
+}
+
+} // extern "C"

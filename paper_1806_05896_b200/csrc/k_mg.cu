@@ -1,0 +1,578 @@
+// Geometric multigrid kernels (sm_100a, FP64): colour Gauss-Seidel sweeps,
+// fused residual + restriction, prolongation, Galerkin RAP, coarse LU and the
+// single-CTA bottom solver.
+//
+// Reference semantics (multigrid.cpp):
+//   bilinear_prolongation  :10-42   P (1D weights 1/2,1,1/2; Dirichlet dropped), R = P^T
+//   gauss_seidel_sweep     :44-66   x_i = (b_i - sum_{j!=i} a_ij x_j) / a_ii
+//   MgHierarchy::build     :75-109  Galerkin R A P down to level 2 (or rediscretised base)
+//   cycle                  :111-132 pre sweeps, restrict residual, recurse, prolong, post
+//   solve                  :141-157 cycles from x=0, throw if ||r|| > 10 ||r_prev||
+// The smoother is a 4-colour symmetric Gauss-Seidel (colour = (gx&1) + 2(gy&1),
+// forward 0..3 / backward 3..0), the GPU-parallel replacement for the
+// lexicographic sweep: it keeps the V-cycle SPD for
+// symmetric operators, which MINRES with P_D requires.
+#include "kernels.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace ocb {
+
+namespace {
+
+__device__ __forceinline__ double prolong_at(const double* __restrict__ ec, int nxc, int gx, int gy)
+{
+    // P row of fine node (gx, gy): coarse parents in ascending column order.
+    int px[2], py[2];
+    double wx[2], wy[2];
+    int cxn = 0, cyn = 0;
+    if (gx & 1) { px[0] = (gx - 1) >> 1; wx[0] = 1.0; cxn = 1; }
+    else {
+        if (gx / 2 - 1 >= 0) { px[cxn] = gx / 2 - 1; wx[cxn++] = 0.5; }
+        if (gx / 2 < nxc) { px[cxn] = gx / 2; wx[cxn++] = 0.5; }
+    }
+    if (gy & 1) { py[0] = (gy - 1) >> 1; wy[0] = 1.0; cyn = 1; }
+    else {
+        if (gy / 2 - 1 >= 0) { py[cyn] = gy / 2 - 1; wy[cyn++] = 0.5; }
+        if (gy / 2 < nxc) { py[cyn] = gy / 2; wy[cyn++] = 0.5; }
+    }
+    double e = 0.0;
+    for (int a = 0; a < cyn; ++a)
+        for (int c = 0; c < cxn; ++c) e += (wx[c] * wy[a]) * ec[(long long)py[a] * nxc + px[c]];
+    return e;
+}
+
+__device__ __forceinline__ double diag_at(const Op9& A, long long i, long long n)
+{
+    double a = A.coef ? A.coef[4 * n + i] : A.c[4];
+    if (A.diag) a += A.diag[i];
+    return a;
+}
+
+// ------------------------------------------------------------------ sweeps
+// Out-of-place: reads x_in (with halo), writes x_out on the tile. In-place
+// would race with neighbouring CTAs that read their halo from this tile.
+template <int TX, int TY, int NS>
+__global__ void __launch_bounds__(256) k_gs_sweep(Op9 A, const double* __restrict__ b,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ xo,
+                                                  const double* __restrict__ ec, int forward,
+                                                  int zero_init)
+{
+    constexpr int H = 4 * NS;
+    constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
+    extern __shared__ double sm[];
+    double* xs = sm;
+    double* bs = xs + RX * RY;
+    double* as = bs + RX * RY;
+
+    const int nx = A.nx;
+    const long long n = (long long)nx * nx;
+    const int nxc = (nx - 1) / 2;
+    const int tx0 = blockIdx.x * TX, ty0 = blockIdx.y * TY;
+    const int ox = tx0 - H, oy = ty0 - H;
+
+    for (int t = threadIdx.x; t < RX * RY; t += blockDim.x) {
+        const int gx = ox + t % RX, gy = oy + t / RX;
+        double xv = 0.0, bv = 0.0, av = 1.0;
+        if (gx >= 0 && gx < nx && gy >= 0 && gy < nx) {
+            const long long i = (long long)gy * nx + gx;
+            xv = zero_init ? 0.0 : x[i];
+            if (ec) xv = xv + prolong_at(ec, nxc, gx, gy); // axpy(1.0, P ec, x)
+            bv = b[i];
+            av = diag_at(A, i, n);
+        }
+        xs[t] = xv;
+        bs[t] = bv;
+        as[t] = av;
+    }
+    __syncthreads();
+
+    constexpr int P = 4 * NS;
+    for (int q = 0; q < P; ++q) {
+        const int pcol = q & 3;
+        const int c = forward ? pcol : 3 - pcol;
+        const int cx = c & 1, cy = c >> 1;
+        const int grow = P - 1 - q;
+        const int lox = max(tx0 - grow, 0), hix = min(tx0 + TX + grow, nx);
+        const int loy = max(ty0 - grow, 0), hiy = min(ty0 + TY + grow, nx);
+        const int gx0 = lox + (((lox & 1) != cx) ? 1 : 0);
+        const int gy0 = loy + (((loy & 1) != cy) ? 1 : 0);
+        const int cntx = hix > gx0 ? (hix - gx0 + 1) / 2 : 0;
+        const int cnty = hiy > gy0 ? (hiy - gy0 + 1) / 2 : 0;
+        for (int idx = threadIdx.x; idx < cntx * cnty; idx += blockDim.x) {
+            const int gx = gx0 + 2 * (idx % cntx), gy = gy0 + 2 * (idx / cntx);
+            const int l = (gy - oy) * RX + (gx - ox);
+            const long long i = (long long)gy * nx + gx;
+            double s = bs[l];
+#pragma unroll
+            for (int d = 0; d < 9; ++d) {
+                if (d == 4) continue;
+                const double a = A.coef ? A.coef[d * n + i] : A.c[d];
+                s -= a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
+            }
+            xs[l] = s / as[l];
+        }
+        __syncthreads();
+    }
+
+    for (int t = threadIdx.x; t < TX * TY; t += blockDim.x) {
+        const int gx = tx0 + t % TX, gy = ty0 + t / TX;
+        if (gx < nx && gy < nx) xo[(long long)gy * nx + gx] = xs[(gy - oy) * RX + (gx - ox)];
+    }
+}
+
+template <int TX, int TY, int NS>
+void sweep_launch(cudaStream_t s, const Op9& A, const double* b, const double* x, double* xo,
+                  bool forward, bool zero_init, const double* ec)
+{
+    constexpr int H = 4 * NS;
+    constexpr size_t smem = 3ull * (TX + 2 * H) * (TY + 2 * H) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_gs_sweep<TX, TY, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
+    k_gs_sweep<TX, TY, NS><<<grid, 256, smem, s>>>(A, b, x, xo, ec, forward ? 1 : 0,
+                                                  zero_init ? 1 : 0);
+}
+
+// --------------------------------------------------------- residual/restrict
+template <int CX, int CY>
+__global__ void __launch_bounds__(CX* CY) k_residual_restrict(Op9 A, const double* __restrict__ b,
+                                                              const double* __restrict__ x,
+                                                              double* __restrict__ bc,
+                                                              double* __restrict__ xc)
+{
+    constexpr int FX = 2 * CX + 1, FY = 2 * CY + 1;
+    __shared__ double rs[FY * FX];
+    const int nx = A.nx;
+    const long long n = (long long)nx * nx;
+    const int nxc = (nx - 1) / 2;
+    const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY;
+    const int fx0 = 2 * cx0, fy0 = 2 * cy0;
+    for (int t = threadIdx.x; t < FX * FY; t += blockDim.x) {
+        const int gx = fx0 + t % FX, gy = fy0 + t / FX;
+        double r = 0.0;
+        if (gx < nx && gy < nx) {
+            const long long i = (long long)gy * nx + gx;
+            // multigrid.cpp:120-121: r = A x; r = rhs - r
+            r = b[i] - op_apply_at(A, x, gx, gy);
+        }
+        rs[t] = r;
+    }
+    __syncthreads();
+    const int cx = cx0 + threadIdx.x % CX, cy = cy0 + threadIdx.x / CX;
+    if (cx < nxc && cy < nxc) {
+        double s = 0.0;
+        // R row = P column: fine (2c..2c+2)^2 in ascending fine index order
+        for (int a = 0; a < 3; ++a) {
+            const double wy = (a == 1) ? 1.0 : 0.5;
+            for (int c = 0; c < 3; ++c) {
+                const double wx = (c == 1) ? 1.0 : 0.5;
+                s += (wx * wy) * rs[(2 * (cy - cy0) + a) * FX + 2 * (cx - cx0) + c];
+            }
+        }
+        const long long I = (long long)cy * nxc + cx;
+        bc[I] = s;
+        if (xc) xc[I] = 0.0; // coarse correction starts from 0 (multigrid.cpp:125)
+    }
+}
+
+__global__ void k_prolong_add(int nx, const double* __restrict__ ec, double* __restrict__ x)
+{
+    const long long n = (long long)nx * nx;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int gx = (int)(i % nx), gy = (int)(i / nx);
+    x[i] = x[i] + prolong_at(ec, (nx - 1) / 2, gx, gy);
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_resid_norm_partials(Op9 A,
+                                                                     const double* __restrict__ b,
+                                                                     const double* __restrict__ x,
+                                                                     double* __restrict__ part)
+{
+    __shared__ double sh[32];
+    const int nx = A.nx;
+    const long long n = (long long)nx * nx;
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int gx = (int)(i % nx), gy = (int)(i / nx);
+        const double r = b[i] - op_apply_at(A, x, gx, gy);
+        acc += r * r;
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_sq_partials(const double* __restrict__ v,
+                                                             long long n, double* __restrict__ part)
+{
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        acc += v[i] * v[i];
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void k_mg_check(const double* __restrict__ part, double* state, int* flags, int init)
+{
+    const double s = sum_partials_warp(part, kRedBlocks);
+    if (threadIdx.x == 0) {
+        const double res = sqrt(s);
+        if (!init && res > 10.0 * state[0]) atomicOr(flags, kErrMgDiverged);
+        state[0] = res;
+    }
+}
+
+// ----------------------------------------------------------------- Galerkin
+__device__ __forceinline__ int parents(int g, int nc, int* p, double* w)
+{
+    if (g & 1) { p[0] = (g - 1) >> 1; w[0] = 1.0; return 1; }
+    int k = 0;
+    if (g / 2 - 1 >= 0) { p[k] = g / 2 - 1; w[k++] = 0.5; }
+    if (g / 2 < nc) { p[k] = g / 2; w[k++] = 0.5; }
+    return k;
+}
+
+__global__ void k_rap(Op9 A, double* __restrict__ coarse, const double* __restrict__ base,
+                      double* __restrict__ rem_out, long long fcs, long long fds, long long ccs)
+{
+    const int nxf = A.nx, nxc = (nxf - 1) / 2;
+    const long long nf = (long long)nxf * nxf, nc = (long long)nxc * nxc;
+    const long long C = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (C >= nc) return;
+    const int bt = blockIdx.y;
+    const double* coef = A.coef ? A.coef + bt * fcs : nullptr;
+    const double* dg = A.diag ? A.diag + bt * fds : nullptr;
+    const int cx = (int)(C % nxc), cy = (int)(C / nxc);
+    double acc[9];
+#pragma unroll
+    for (int d = 0; d < 9; ++d) acc[d] = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        const int fy = 2 * cy + a;
+        const double wyf = (a == 1) ? 1.0 : 0.5;
+        for (int c = 0; c < 3; ++c) {
+            const int fx = 2 * cx + c;
+            const double wf = ((c == 1) ? 1.0 : 0.5) * wyf;
+            const long long fi = (long long)fy * nxf + fx;
+            for (int d = 0; d < 9; ++d) {
+                const int gx = fx + d % 3 - 1, gy = fy + d / 3 - 1;
+                if (gx < 0 || gx >= nxf || gy < 0 || gy >= nxf) continue;
+                double av = coef ? coef[d * nf + fi] : A.c[d];
+                if (d == 4 && dg) av += dg[fi];
+                if (av == 0.0) continue;
+                int pxs[2], pys[2];
+                double wxs[2], wys[2];
+                const int npx = parents(gx, nxc, pxs, wxs), npy = parents(gy, nxc, pys, wys);
+                for (int u = 0; u < npy; ++u)
+                    for (int v = 0; v < npx; ++v) {
+                        const int D = (pys[u] - cy + 1) * 3 + (pxs[v] - cx + 1);
+                        acc[D] += wf * av * (wxs[v] * wys[u]);
+                    }
+            }
+        }
+    }
+    double* out = coarse + bt * ccs;
+    // rediscretised levels (multigrid.cpp:94-96): coarse = base + R rem P, and
+    // the Galerkin remainder itself is carried to the next level
+#pragma unroll
+    for (int d = 0; d < 9; ++d) out[d * nc + C] = base ? base[d * nc + C] + acc[d] : acc[d];
+    if (rem_out) {
+        double* ro = rem_out + bt * ccs;
+#pragma unroll
+        for (int d = 0; d < 9; ++d) ro[d * nc + C] = acc[d];
+    }
+}
+
+__global__ void k_remainder9(Op9 A, const double* __restrict__ base, double* __restrict__ rem)
+{
+    const long long n = (long long)A.nx * A.nx;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) {
+        double a = A.coef ? A.coef[d * n + i] : A.c[d];
+        if (d == 4 && A.diag) a += A.diag[i];
+        rem[d * n + i] = a - base[d * n + i];
+    }
+}
+
+__global__ void k_coarse_lu(const double* __restrict__ coef9, double* __restrict__ lu,
+                            int* __restrict__ perm, long long cstride)
+{
+    // dense 9x9 from the level-2 (nx = 3) 9-point arrays, column-major
+    const int bt = blockIdx.x;
+    const double* cf = coef9 + bt * cstride;
+    double a[81];
+    for (int k = 0; k < 81; ++k) a[k] = 0.0;
+    for (int i = 0; i < 9; ++i) {
+        const int gx = i % 3, gy = i / 3;
+        for (int d = 0; d < 9; ++d) {
+            const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
+            if (jx < 0 || jx >= 3 || jy < 0 || jy >= 3) continue;
+            a[(jy * 3 + jx) * 9 + i] = cf[d * 9 + i];
+        }
+    }
+    int pm[9];
+    for (int i = 0; i < 9; ++i) pm[i] = i;
+    for (int k = 0; k < 9; ++k) {
+        int piv = k;
+        double best = fabs(a[k * 9 + k]);
+        for (int i = k + 1; i < 9; ++i)
+            if (fabs(a[k * 9 + i]) > best) { best = fabs(a[k * 9 + i]); piv = i; }
+        if (piv != k) {
+            for (int j = 0; j < 9; ++j) {
+                const double t = a[j * 9 + k];
+                a[j * 9 + k] = a[j * 9 + piv];
+                a[j * 9 + piv] = t;
+            }
+            const int t = pm[k]; pm[k] = pm[piv]; pm[piv] = t;
+        }
+        const double p = a[k * 9 + k];
+        if (p == 0.0) continue;
+        for (int i = k + 1; i < 9; ++i) a[k * 9 + i] /= p;
+        for (int j = k + 1; j < 9; ++j) {
+            const double u = a[j * 9 + k];
+            if (u == 0.0) continue;
+            for (int i = k + 1; i < 9; ++i) a[j * 9 + i] -= a[k * 9 + i] * u;
+        }
+    }
+    for (int k = 0; k < 81; ++k) lu[bt * 81 + k] = a[k];
+    for (int i = 0; i < 9; ++i) perm[bt * 9 + i] = pm[i];
+}
+
+// ----------------------------------------------------------- bottom solver
+constexpr int kBottomThreads = 1024;
+
+__device__ void bt_sweep(const Op9& A, const double* bsm, double* xsm, bool forward)
+{
+    const int nx = A.nx;
+    const long long n = (long long)nx * nx;
+    for (int p = 0; p < 4; ++p) {
+        const int c = forward ? p : 3 - p;
+        const int cx = c & 1, cy = c >> 1;
+        const int cntx = (nx - cx + 1) / 2, cnty = (nx - cy + 1) / 2;
+        for (int idx = threadIdx.x; idx < cntx * cnty; idx += blockDim.x) {
+            const int gx = cx + 2 * (idx % cntx), gy = cy + 2 * (idx / cntx);
+            const long long i = (long long)gy * nx + gx;
+            double s = bsm[i];
+#pragma unroll
+            for (int d = 0; d < 9; ++d) {
+                if (d == 4) continue;
+                const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
+                if (jx < 0 || jx >= nx || jy < 0 || jy >= nx) continue;
+                const double a = A.coef ? A.coef[d * n + i] : A.c[d];
+                s -= a * xsm[(long long)jy * nx + jx];
+            }
+            xsm[i] = s / diag_at(A, i, n);
+        }
+        __syncthreads();
+    }
+}
+
+__device__ double bt_resid_sq(const Op9& A, const double* bsm, const double* xsm, double* red)
+{
+    const int nx = A.nx;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nx * nx; i += blockDim.x) {
+        const double r = bsm[i] - op_apply_at(A, xsm, i % nx, i / nx);
+        acc += r * r;
+    }
+    acc = block_sum(acc, red);
+    __syncthreads();
+    if (threadIdx.x == 0) red[32] = acc;
+    __syncthreads();
+    const double out = red[32];
+    __syncthreads();
+    return out;
+}
+
+__global__ void __launch_bounds__(kBottomThreads) k_bottom(BottomArgs a, const double* __restrict__ bg,
+                                                           double* __restrict__ xg, int cycles,
+                                                           int pre, int post, int check,
+                                                           double* state, int* flags)
+{
+    extern __shared__ double sm[];
+    __shared__ double red[40];
+    double* xs[kBottomMaxLevels];
+    double* bs[kBottomMaxLevels];
+    double* p = sm;
+    for (int k = 0; k < a.nlev; ++k) {
+        const int m = a.ops[k].nx * a.ops[k].nx;
+        xs[k] = p; p += m;
+        bs[k] = p; p += m;
+    }
+    double* rs = p;
+    const int n0 = a.ops[0].nx * a.ops[0].nx;
+    for (int i = threadIdx.x; i < n0; i += blockDim.x) {
+        bs[0][i] = bg[i];
+        xs[0][i] = 0.0;
+    }
+    __syncthreads();
+    double prev = 0.0;
+    if (check) {
+        double acc = 0.0;
+        for (int i = threadIdx.x; i < n0; i += blockDim.x) acc += bs[0][i] * bs[0][i];
+        acc = block_sum(acc, red);
+        __syncthreads();
+        if (threadIdx.x == 0) red[32] = sqrt(acc);
+        __syncthreads();
+        prev = red[32];
+        __syncthreads();
+    }
+    const int last = a.nlev - 1;
+    for (int cyc = 0; cyc < cycles; ++cyc) {
+        for (int k = 0; k < last; ++k) {
+            const Op9& A = a.ops[k];
+            for (int s = 0; s < pre; ++s) bt_sweep(A, bs[k], xs[k], true);
+            const int nx = A.nx, nxc = (nx - 1) / 2;
+            for (int i = threadIdx.x; i < nx * nx; i += blockDim.x)
+                rs[i] = bs[k][i] - op_apply_at(A, xs[k], i % nx, i / nx);
+            __syncthreads();
+            for (int I = threadIdx.x; I < nxc * nxc; I += blockDim.x) {
+                const int cx = I % nxc, cy = I / nxc;
+                double s = 0.0;
+                for (int u = 0; u < 3; ++u) {
+                    const double wy = (u == 1) ? 1.0 : 0.5;
+                    for (int v = 0; v < 3; ++v) {
+                        const double wx = (v == 1) ? 1.0 : 0.5;
+                        s += (wx * wy) * rs[(2 * cy + u) * nx + 2 * cx + v];
+                    }
+                }
+                bs[k + 1][I] = s;
+                xs[k + 1][I] = 0.0;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            // level-2 dense LU solve (DenseFactor::solve)
+            double y[9];
+            for (int i = 0; i < 9; ++i) y[i] = bs[last][a.perm[i]];
+            for (int i = 0; i < 9; ++i)
+                for (int k = 0; k < i; ++k) y[i] -= a.lu[k * 9 + i] * y[k];
+            for (int i = 8; i >= 0; --i) {
+                for (int k = i + 1; k < 9; ++k) y[i] -= a.lu[k * 9 + i] * y[k];
+                y[i] /= a.lu[i * 9 + i];
+            }
+            for (int i = 0; i < 9; ++i) xs[last][i] = y[i];
+        }
+        __syncthreads();
+        for (int k = last - 1; k >= 0; --k) {
+            const Op9& A = a.ops[k];
+            const int nx = A.nx, nxc = (nx - 1) / 2;
+            for (int i = threadIdx.x; i < nx * nx; i += blockDim.x)
+                xs[k][i] = xs[k][i] + prolong_at(xs[k + 1], nxc, i % nx, i / nx);
+            __syncthreads();
+            for (int s = 0; s < post; ++s) bt_sweep(A, bs[k], xs[k], false);
+        }
+        if (check) {
+            const double res = sqrt(bt_resid_sq(a.ops[0], bs[0], xs[0], red));
+            if (threadIdx.x == 0 && res > 10.0 * prev) atomicOr(flags, kErrMgDiverged);
+            prev = res;
+        }
+    }
+    for (int i = threadIdx.x; i < n0; i += blockDim.x) xg[i] = xs[0][i];
+    if (check && threadIdx.x == 0 && state) state[0] = prev;
+}
+
+} // namespace
+
+// ------------------------------------------------------------- launchers
+void launch_gs_sweep(cudaStream_t s, const Op9& A, const double* b, const double* x, double* xo,
+                     bool forward, bool zero_init, const double* ec, int sweeps_fused)
+{
+    if (sweeps_fused == 2) {
+        if (A.nx >= 1000) sweep_launch<64, 32, 2>(s, A, b, x, xo, forward, zero_init, ec);
+        else if (A.nx >= 500) sweep_launch<32, 32, 2>(s, A, b, x, xo, forward, zero_init, ec);
+        else sweep_launch<32, 16, 2>(s, A, b, x, xo, forward, zero_init, ec);
+        return;
+    }
+    if (A.nx >= 1000) sweep_launch<64, 32, 1>(s, A, b, x, xo, forward, zero_init, ec);
+    else if (A.nx >= 500) sweep_launch<32, 32, 1>(s, A, b, x, xo, forward, zero_init, ec);
+    else if (A.nx >= 200) sweep_launch<32, 16, 1>(s, A, b, x, xo, forward, zero_init, ec);
+    else sweep_launch<16, 16, 1>(s, A, b, x, xo, forward, zero_init, ec);
+}
+
+void launch_residual_restrict(cudaStream_t s, const Op9& A, const double* b, const double* x,
+                              double* bc, double* xc)
+{
+    constexpr int CX = 32, CY = 8;
+    const int nxc = (A.nx - 1) / 2;
+    dim3 grid((nxc + CX - 1) / CX, (nxc + CY - 1) / CY);
+    k_residual_restrict<CX, CY><<<grid, CX * CY, 0, s>>>(A, b, x, bc, xc);
+}
+
+void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x)
+{
+    const long long n = (long long)nx * nx;
+    k_prolong_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nx, ec, x);
+}
+
+void launch_residual_norm_partials(cudaStream_t s, const Op9& A, const double* b,
+                                   const double* x, double* part)
+{
+    k_resid_norm_partials<<<kRedBlocks, kRedThreads, 0, s>>>(A, b, x, part);
+}
+
+void launch_mg_check(cudaStream_t s, const double* part, double* state, int* flags)
+{
+    k_mg_check<<<1, 32, 0, s>>>(part, state, flags, 0);
+}
+
+void launch_norm_init(cudaStream_t s, const double* b, long long n, double* part, double* state)
+{
+    k_sq_partials<<<kRedBlocks, kRedThreads, 0, s>>>(b, n, part);
+    k_mg_check<<<1, 32, 0, s>>>(part, state, nullptr, 1);
+}
+
+void launch_rap(cudaStream_t s, const Op9& fine, double* coarse, const double* base,
+                double* rem_out, int batch, long long fcs, long long fds, long long ccs)
+{
+    const int nxc = (fine.nx - 1) / 2;
+    const long long nc = (long long)nxc * nxc;
+    dim3 grid((unsigned)((nc + 127) / 128), batch);
+    k_rap<<<grid, 128, 0, s>>>(fine, coarse, base, rem_out, fcs, fds, ccs);
+}
+
+void launch_remainder9(cudaStream_t s, const Op9& fine, const double* base9, double* rem9)
+{
+    const long long n = (long long)fine.nx * fine.nx;
+    k_remainder9<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(fine, base9, rem9);
+}
+
+void launch_coarse_lu(cudaStream_t s, const double* coef9, double* lu, int* perm, int batch)
+{
+    k_coarse_lu<<<batch, 1, 0, s>>>(coef9, lu, perm, 81);
+}
+
+size_t bottom_smem_bytes(const BottomArgs& a)
+{
+    size_t m = 0;
+    for (int k = 0; k < a.nlev; ++k) m += 2ull * a.ops[k].nx * a.ops[k].nx;
+    m += (size_t)a.ops[0].nx * a.ops[0].nx;
+    return m * sizeof(double);
+}
+
+void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double* x, int cycles,
+                   int pre, int post, bool check, double* state, int* flags)
+{
+    const size_t smem = bottom_smem_bytes(a);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    if (smem > 200 * 1024) throw std::runtime_error("bottom solver: level too large for one CTA");
+    k_bottom<<<1, kBottomThreads, smem, s>>>(a, b, x, cycles, pre, post, check ? 1 : 0, state,
+                                             flags);
+}
+
+} // namespace ocb

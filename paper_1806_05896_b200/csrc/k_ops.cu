@@ -1,0 +1,424 @@
+// Saddle-operator and preconditioner-block kernels (sm_100a, FP64).
+//
+// Each kernel is one pass over the grid with the 9-point stencils applied
+// matrix-free (constant L, M, M+tau L) or from 9 coefficient arrays (SUPG
+// convection-diffusion, partial observation mass). Arithmetic follows the
+// reference's evaluation order term by term so results agree to rounding.
+#include "kernels.hpp"
+
+namespace ocb {
+
+namespace {
+
+constexpr int kT = 256;
+
+inline unsigned blocks_for(long long n) { return (unsigned)((n + kT - 1) / kT); }
+
+__device__ __forceinline__ double stencil_diff(const Op9& A, const double* __restrict__ w,
+                                               const double* __restrict__ v, int gx, int gy)
+{
+    // (A (w - v))_i with the difference formed per entry first (qp.cpp:84-87)
+    const int nx = A.nx;
+    const long long n = (long long)nx * nx;
+    const long long i = (long long)gy * nx + gx;
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) {
+        const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
+        if (jx < 0 || jx >= nx || jy < 0 || jy >= nx) continue;
+        const long long j = (long long)jy * nx + jx;
+        s += op_coef(A, d, i, n) * (w[j] - v[j]);
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------- KKT (steady)
+// make_saddle_operator (ipm.cpp:244-267) over steady_matvecs (ipm.cpp:347-374):
+//   ry = (M_obs y + th_y y) + L^T p
+//   rw = (alpha M(w-v) + th_w w) - M p
+//   rv = (alpha (-M(w-v)) + th_v v) + M p
+//   rp = L y - M(w-v)
+template <bool HAS_TY, bool RESID>
+__global__ void __launch_bounds__(kT) k_kkt_steady(ProbDev P, const double* __restrict__ ty,
+                                                   const double* __restrict__ tw,
+                                                   const double* __restrict__ tv,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ out,
+                                                   const double* __restrict__ b,
+                                                   double* __restrict__ part)
+{
+    __shared__ double sh[32];
+    const long long n = P.ns;
+    const int nx = P.nx;
+    const double* y = x;
+    const double* w = x + n;
+    const double* v = x + 2 * n;
+    const double* p = x + 3 * n;
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int gx = (int)(i % nx), gy = (int)(i / nx);
+        const double My = op_apply_at(P.Mobs, y, gx, gy);
+        const double Ltp = op_apply_at(P.LT, p, gx, gy);
+        const double Mwv = stencil_diff(P.M, w, v, gx, gy);
+        const double Mp = op_apply_at(P.M, p, gx, gy);
+        const double Ly = op_apply_at(P.L, y, gx, gy);
+        double ry = My;
+        if (HAS_TY) ry += ty[i] * y[i];
+        ry = ry + Ltp;
+        const double rw = (P.alpha * Mwv + tw[i] * w[i]) - Mp;
+        const double rv = (P.alpha * (-Mwv) + tv[i] * v[i]) + Mp;
+        const double rp = Ly - Mwv;
+        if (RESID) {
+            const double d0 = b[i] - ry, d1 = b[n + i] - rw, d2 = b[2 * n + i] - rv,
+                         d3 = b[3 * n + i] - rp;
+            acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+        }
+        if (out) {
+            out[i] = ry;
+            out[n + i] = rw;
+            out[2 * n + i] = rv;
+            out[3 * n + i] = rp;
+        }
+    }
+    if (RESID) {
+        acc = block_sum(acc, sh);
+        if (threadIdx.x == 0) part[blockIdx.x] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ KKT (heat)
+// space-time blocks (timedep.cpp:18-133), block k of ns nodes, s_k = tau w_k:
+//   hy = s_k (M y_k);  K y = Mtl y_k - M y_{k-1};  K^T p = Mtl p_k - M p_{k+1}
+//   hz = [a_k M(w-v); -a_k M(w-v)], a_k = alpha tau w_k;  B z = tau (M(w-v))
+//   B^T p = [tau (M p); -tau (M p)]
+template <bool HAS_TY, bool RESID>
+__global__ void __launch_bounds__(kT) k_kkt_heat(ProbDev P, const double* __restrict__ ty,
+                                                 const double* __restrict__ tw,
+                                                 const double* __restrict__ tv,
+                                                 const double* __restrict__ x,
+                                                 double* __restrict__ out,
+                                                 const double* __restrict__ b,
+                                                 double* __restrict__ part)
+{
+    __shared__ double sh[32];
+    const long long ns = P.ns, N = P.ny;
+    const int nx = P.nx;
+    const double* y = x;
+    const double* w = x + N;
+    const double* v = x + 2 * N;
+    const double* p = x + 3 * N;
+    double acc = 0.0;
+    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < N;
+         g += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(g / ns);
+        const long long i = g - (long long)k * ns;
+        const int gx = (int)(i % nx), gy = (int)(i / nx);
+        const long long off = (long long)k * ns;
+        const double sk = P.tau * P.qw[k];
+        const double ak = P.alpha * P.tau * P.qw[k];
+        const double hy = sk * op_apply_at(P.M, y + off, gx, gy);
+        double ktp = op_apply_at(P.Mtl, p + off, gx, gy);
+        if (k + 1 < P.nt) ktp -= op_apply_at(P.M, p + off + ns, gx, gy);
+        double ky = op_apply_at(P.Mtl, y + off, gx, gy);
+        if (k > 0) ky -= op_apply_at(P.M, y + off - ns, gx, gy);
+        const double Mwv = stencil_diff(P.M, w + off, v + off, gx, gy);
+        const double Mp = op_apply_at(P.M, p + off, gx, gy);
+        double ry = hy;
+        if (HAS_TY) ry += ty[g] * y[g];
+        ry = ry + ktp;
+        const double rw = (ak * Mwv + tw[g] * w[g]) - P.tau * Mp;
+        const double rv = ((-ak) * Mwv + tv[g] * v[g]) + P.tau * Mp;
+        const double rp = ky - P.tau * Mwv;
+        if (RESID) {
+            const double d0 = b[g] - ry, d1 = b[N + g] - rw, d2 = b[2 * N + g] - rv,
+                         d3 = b[3 * N + g] - rp;
+            acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+        }
+        if (out) {
+            out[g] = ry;
+            out[N + g] = rw;
+            out[2 * N + g] = rv;
+            out[3 * N + g] = rp;
+        }
+    }
+    if (RESID) {
+        acc = block_sum(acc, sh);
+        if (threadIdx.x == 0) part[blockIdx.x] = acc;
+    }
+}
+
+// ------------------------------------------------------------------- Chebyshev
+// ChebyshevSemiIteration (chebyshev.cpp:9-75) on s_k M + diag(e), Jacobi
+// scaled with the fixed interval [1/4, 9/4]: omega = 0.8, rho = 0.8.
+__device__ __forceinline__ double cheb_invd(const ProbDev& P, const double* e, int k, long long g)
+{
+    const double sk = P.heat ? P.tau * P.qw[k] : 1.0;
+    const double di = sk * P.M.c[4] + (e ? e[g] : 0.0);
+    return 1.0 / di;
+}
+
+__global__ void k_cheb_init(ProbDev P, const double* __restrict__ b, const double* __restrict__ e,
+                            double omega, double* __restrict__ g_out)
+{
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= P.ny) return;
+    const int k = (int)(g / P.ns);
+    g_out[g] = omega * cheb_invd(P, e, k, g) * b[g];
+}
+
+__global__ void k_cheb_step(ProbDev P, const double* __restrict__ e, double omega, double wk,
+                            const double* __restrict__ prev, const double* __restrict__ cur,
+                            const double* __restrict__ gv, double* __restrict__ next)
+{
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= P.ny) return;
+    const long long ns = P.ns;
+    const int k = (int)(g / ns);
+    const long long i = g - (long long)k * ns;
+    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    double az = op_apply_at(P.M, cur + (long long)k * ns, gx, gy);
+    if (P.heat) az = (P.tau * P.qw[k]) * az; // matvec: scale only when scale != 1
+    if (e) az += e[g] * cur[g];
+    const double invd = cheb_invd(P, e, k, g);
+    const double s_cur = cur[g] - omega * invd * az;
+    const double pv = prev ? prev[g] : 0.0;
+    next[g] = wk * (s_cur + gv[g] - pv) + pv;
+}
+
+// ------------------------------------------------------------------ 2x2 block
+__global__ void k_control_2x2(ProbDev P, const double* __restrict__ tw,
+                              const double* __restrict__ tv, const double* __restrict__ rw,
+                              const double* __restrict__ rv, double* __restrict__ vw,
+                              double* __restrict__ vv, int* flags)
+{
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= P.ny) return;
+    const int k = (int)(g / P.ns);
+    const double dM = P.M.c[4];
+    const double sc = P.heat ? P.alpha * P.tau * P.qw[k] : P.alpha;
+    const double a = sc * dM + tw[g];
+    const double bb = -sc * dM;
+    const double c = sc * dM + tv[g];
+    if (a == 0.0) { atomicOr(flags, kErrSingular2x2); return; }
+    const double schur = c - bb * bb / a;
+    if (schur == 0.0) { atomicOr(flags, kErrSingular2x2); return; }
+    const double x2 = (rv[g] - bb * rw[g] / a) / schur;
+    const double x1 = (rw[g] - bb * x2) / a;
+    vw[g] = x1;
+    vv[g] = x2;
+}
+
+// -------------------------------------------------------------- coupling rows
+__global__ void k_coupling_steady(ProbDev P, const double* __restrict__ vy,
+                                  const double* __restrict__ vw, const double* __restrict__ vv,
+                                  const double* __restrict__ rp, double* __restrict__ t)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const double Lvy = op_apply_at(P.L, vy, gx, gy);
+    const double mw = op_apply_at(P.M, vw, gx, gy);
+    const double mv = op_apply_at(P.M, vv, gx, gy);
+    t[i] = Lvy + ((-mw + mv) - rp[i]);
+}
+
+__global__ void k_coupling_heat(ProbDev P, const double* __restrict__ vy,
+                                const double* __restrict__ vw, const double* __restrict__ vv,
+                                const double* __restrict__ rp, double* __restrict__ t)
+{
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= P.ny) return;
+    const long long ns = P.ns;
+    const int k = (int)(g / ns);
+    const long long i = g - (long long)k * ns;
+    const long long off = (long long)k * ns;
+    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    double ly = op_apply_at(P.Mtl, vy + off, gx, gy);
+    if (k > 0) ly -= op_apply_at(P.M, vy + off - ns, gx, gy);
+    const double cz = P.tau * stencil_diff(P.M, vw + off, vv + off, gx, gy);
+    t[g] = ly + (-cz - rp[g]);
+}
+
+__global__ void k_schur_middle(ProbDev P, const double* __restrict__ ty,
+                               const double* __restrict__ t1, double* __restrict__ t2)
+{
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= P.ny) return;
+    const long long ns = P.ns;
+    const int k = (int)(g / ns);
+    const long long i = g - (long long)k * ns;
+    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const double tyv = ty ? ty[g] : 0.0;
+    if (P.heat) {
+        const double m = op_apply_at(P.M, t1 + (long long)k * ns, gx, gy);
+        t2[g] = (P.tau * P.qw[k]) * m + tyv * t1[g];
+    } else {
+        double m = op_apply_at(P.Mobs, t1, gx, gy);
+        if (ty) m += tyv * t1[g];
+        t2[g] = m;
+    }
+}
+
+__global__ void k_ppi_rhs1(ProbDev P, const double* __restrict__ vw, const double* __restrict__ vv,
+                           const double* __restrict__ rp, double* __restrict__ rhs1)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    rhs1[i] = stencil_diff(P.M, vw, vv, gx, gy) + rp[i];
+}
+
+__global__ void k_ppi_t(ProbDev P, const double* __restrict__ ty, const double* __restrict__ v1,
+                        const double* __restrict__ ry, double* __restrict__ t)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const double tyv = ty ? ty[i] : 0.0;
+    t[i] = op_apply_at(P.Mobs, v1, gx, gy) + (tyv * v1[i] - ry[i]);
+}
+
+__global__ void k_op_apply(Op9 A, const double* __restrict__ x, double* __restrict__ y)
+{
+    const long long n = (long long)A.nx * A.nx;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    y[i] = op_apply_at(A, x, (int)(i % A.nx), (int)(i / A.nx));
+}
+
+__global__ void k_rhs_plus_mass(ProbDev P, const double* __restrict__ r,
+                                const double* __restrict__ xnb, double* __restrict__ rhs)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.ns) return;
+    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    rhs[i] = xnb ? r[i] + op_apply_at(P.M, xnb, gx, gy) : r[i];
+}
+
+__global__ void k_mhat(ProbDev P, const double* __restrict__ ty, const double* __restrict__ tw,
+                       const double* __restrict__ tv, double* __restrict__ mhat,
+                       double* __restrict__ bracket, int* flags)
+{
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= P.ny) return;
+    const double d = P.M.c[4];
+    const double twv = tw[g], tvv = tv[g];
+    const double tyv = ty ? ty[g] : 0.0;
+    if (d <= 0.0 || twv <= 0.0 || tvv <= 0.0 || tyv < 0.0) {
+        atomicOr(flags, kErrBadInput);
+        return;
+    }
+    const double s = 1.0 / twv + 1.0 / tvv;
+    double br;
+    double scale_d;
+    if (P.heat) {
+        const int k = (int)(g / P.ns);
+        const double dc = P.qw[k] * d;
+        br = P.tau * P.tau * d * d * s / (P.alpha * P.tau * dc * s + 1.0);
+        scale_d = P.tau * dc;
+    } else {
+        br = d * d * s / (P.alpha * d * s + 1.0);
+        scale_d = d;
+    }
+    if (br < -1e-14) atomicOr(flags, kErrNegBracket);
+    br = fmax(br, 0.0);
+    if (bracket) bracket[g] = br;
+    if (mhat) mhat[g] = sqrt(br) * sqrt(scale_d + tyv);
+}
+
+} // namespace
+
+void launch_mhat(cudaStream_t s, const ProbDev& P, const double* ty, const double* tw,
+                 const double* tv, double* mhat, double* bracket, int* flags)
+{
+    k_mhat<<<blocks_for(P.ny), kT, 0, s>>>(P, ty, tw, tv, mhat, bracket, flags);
+}
+
+void launch_kkt(cudaStream_t s, const ProbDev& P, const double* ty, const double* tw,
+                const double* tv, const double* x, double* out, const double* b, double* part)
+{
+    const bool has_ty = ty != nullptr;
+    const bool resid = part != nullptr;
+    const long long N = P.ny;
+    const unsigned grid = resid ? kRedBlocks : blocks_for(N);
+    if (P.heat) {
+        if (has_ty && resid) k_kkt_heat<true, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else if (has_ty) k_kkt_heat<true, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else if (resid) k_kkt_heat<false, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else k_kkt_heat<false, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+    } else {
+        if (has_ty && resid) k_kkt_steady<true, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else if (has_ty) k_kkt_steady<true, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else if (resid) k_kkt_steady<false, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else k_kkt_steady<false, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+    }
+}
+
+void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const double* e,
+                      int steps, const ChebWork& w, double* out)
+{
+    const double lmin = 0.25, lmax = 2.25;
+    const double omega = 2.0 / (lmin + lmax);
+    const double rho = (lmax - lmin) / (lmax + lmin);
+    const unsigned grid = blocks_for(P.ny);
+    if (steps <= 1) {
+        k_cheb_init<<<grid, kT, 0, s>>>(P, b, e, omega, out);
+        return;
+    }
+    k_cheb_init<<<grid, kT, 0, s>>>(P, b, e, omega, w.g);
+    // rotating buffers R[s % 3]; the last step (s = steps) writes into out
+    double* R[3] = {w.r0, w.r1, w.r2};
+    R[steps % 3] = out;
+    double wk = 1.0;
+    for (int st = 2; st <= steps; ++st) {
+        wk = (st == 2) ? 1.0 / (1.0 - 0.5 * rho * rho) : 1.0 / (1.0 - 0.25 * rho * rho * wk);
+        const double* prev = (st == 2) ? nullptr : (st == 3 ? w.g : R[(st - 2) % 3]);
+        const double* cur = (st == 2) ? w.g : R[(st - 1) % 3];
+        k_cheb_step<<<grid, kT, 0, s>>>(P, e, omega, wk, prev, cur, w.g, R[st % 3]);
+    }
+}
+
+void launch_control_2x2(cudaStream_t s, const ProbDev& P, const double* tw, const double* tv,
+                        const double* rw, const double* rv, double* vw, double* vv, int* flags)
+{
+    k_control_2x2<<<blocks_for(P.ny), kT, 0, s>>>(P, tw, tv, rw, rv, vw, vv, flags);
+}
+
+void launch_coupling(cudaStream_t s, const ProbDev& P, const double* vy, const double* vw,
+                     const double* vv, const double* rp, double* t)
+{
+    if (P.heat) k_coupling_heat<<<blocks_for(P.ny), kT, 0, s>>>(P, vy, vw, vv, rp, t);
+    else k_coupling_steady<<<blocks_for(P.ns), kT, 0, s>>>(P, vy, vw, vv, rp, t);
+}
+
+void launch_schur_middle(cudaStream_t s, const ProbDev& P, const double* ty, const double* t1,
+                         double* t2)
+{
+    k_schur_middle<<<blocks_for(P.ny), kT, 0, s>>>(P, ty, t1, t2);
+}
+
+void launch_ppi_rhs1(cudaStream_t s, const ProbDev& P, const double* vw, const double* vv,
+                     const double* rp, double* rhs1)
+{
+    k_ppi_rhs1<<<blocks_for(P.ns), kT, 0, s>>>(P, vw, vv, rp, rhs1);
+}
+
+void launch_ppi_t(cudaStream_t s, const ProbDev& P, const double* ty, const double* v1,
+                  const double* ry, double* t)
+{
+    k_ppi_t<<<blocks_for(P.ns), kT, 0, s>>>(P, ty, v1, ry, t);
+}
+
+void launch_op_apply(cudaStream_t s, const Op9& A, const double* x, double* y)
+{
+    k_op_apply<<<blocks_for((long long)A.nx * A.nx), kT, 0, s>>>(A, x, y);
+}
+
+void launch_rhs_plus_mass(cudaStream_t s, const ProbDev& P, const double* r, const double* xnb,
+                          double* rhs)
+{
+    k_rhs_plus_mass<<<blocks_for(P.ns), kT, 0, s>>>(P, r, xnb, rhs);
+}
+
+} // namespace ocb

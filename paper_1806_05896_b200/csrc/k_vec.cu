@@ -1,0 +1,326 @@
+// Krylov vector kernels (sm_100a, FP64): deterministic reductions, the MGS
+// Arnoldi step, GMRES Givens/back-substitution and the MINRES recurrences.
+//
+// Reductions use a fixed grid of kRedBlocks partials summed in a fixed order,
+// so repeated solves are bit-identical (reference kernels.hpp:20-21). The
+// scalar recurrences run in one thread on the device so the host only reads
+// the convergence scalars once per Krylov iteration.
+#include "kernels.hpp"
+
+namespace ocb {
+
+namespace {
+
+constexpr int kT = 256;
+inline unsigned blocks_for(long long n) { return (unsigned)((n + kT - 1) / kT); }
+
+__global__ void __launch_bounds__(kRedThreads) k_dot_partials(const double* __restrict__ x,
+                                                              const double* __restrict__ y,
+                                                              long long n, double* __restrict__ part)
+{
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        acc += x[i] * y[i];
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void k_finalize(const double* __restrict__ part, double* dst, int mode)
+{
+    const double s = sum_partials_warp(part, kRedBlocks);
+    if (threadIdx.x == 0) dst[0] = mode == 1 ? sqrt(s) : s;
+}
+
+__global__ void k_copy(const double* __restrict__ x, double* __restrict__ y, long long n)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = x[i];
+}
+
+__global__ void k_fill(double* __restrict__ x, double v, long long n)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = v;
+}
+
+__global__ void k_scale_inv(const double* x, const double* __restrict__ den, double* y,
+                            long long n, const int* __restrict__ stop)
+{
+    if (stop && *stop) return;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const double d = *den;
+    if (stop && !(d > 1e-300)) return; // GMRES: basis exhausted, V_{j+1} not formed
+    if (i < n) y[i] = x[i] * (1.0 / d);
+}
+
+__global__ void k_axpy_neg(const double* __restrict__ h, const double* __restrict__ v,
+                           double* __restrict__ w, long long n)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) w[i] += (-h[0]) * v[i];
+}
+
+__global__ void k_combine(const double* const* __restrict__ Z, const double* __restrict__ y,
+                          int m, double* __restrict__ x, long long n, const double* __restrict__ xb)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = xb ? xb[i] : 0.0;
+    for (int k = 0; k < m; ++k) acc += y[k] * Z[k][i];
+    x[i] = acc;
+}
+
+__global__ void k_add(const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ out, long long n)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = a[i] + b[i];
+}
+
+__global__ void k_mgs_step(const double* __restrict__ part, double* H, int ld, int i, int j,
+                           const double* __restrict__ vi, double* __restrict__ w, long long n)
+{
+    __shared__ double hs;
+    if (threadIdx.x < 32) {
+        const double s = sum_partials_warp(part, kRedBlocks);
+        if (threadIdx.x == 0) {
+            hs = s;
+            if (blockIdx.x == 0) H[(long long)j * ld + i] = s;
+        }
+    }
+    __syncthreads();
+    const double h = hs;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long long)gridDim.x * blockDim.x)
+        w[k] += (-h) * vi[k];
+}
+
+__global__ void k_gmres_givens(const double* __restrict__ part, GmresDev G, int j)
+{
+    const double s2 = sum_partials_warp(part, kRedBlocks);
+    if (threadIdx.x != 0) return;
+    const double hnext = sqrt(s2);
+    G.scal[1] = hnext;
+    double* h = G.H + (long long)j * G.ld;
+    h[j + 1] = hnext;
+    for (int i = 0; i < j; ++i) {
+        const double t = G.cs[i] * h[i] + G.sn[i] * h[i + 1];
+        h[i + 1] = -G.sn[i] * h[i] + G.cs[i] * h[i + 1];
+        h[i] = t;
+    }
+    const double r = hypot(h[j], hnext);
+    if (r == 0.0) {
+        *G.stop = 1; // "gmres: zero pivot in Hessenberg triangularization"
+        return;
+    }
+    G.cs[j] = h[j] / r;
+    G.sn[j] = hnext / r;
+    h[j] = r;
+    G.g[j + 1] = -G.sn[j] * G.g[j];
+    G.g[j] *= G.cs[j];
+    const int m = j + 1;
+    for (int i = m - 1; i >= 0; --i) {
+        double s = G.g[i];
+        for (int k2 = i + 1; k2 < m; ++k2) s -= G.H[(long long)k2 * G.ld + i] * G.y[k2];
+        G.y[i] = s / G.H[(long long)i * G.ld + i];
+    }
+}
+
+__global__ void k_relres(const double* __restrict__ part, const double* __restrict__ bnorm,
+                         double* dst)
+{
+    const double s = sum_partials_warp(part, kRedBlocks);
+    if (threadIdx.x == 0) dst[0] = sqrt(s) / bnorm[0];
+}
+
+// MINRES scalar slots
+enum {
+    kGamma = 0, kGammaPrev, kEta, kCPrev, kC, kSPrev, kS, kDelta, kGammaNext, kA0, kA1, kA2, kA3,
+    kCNext, kSNext, kGammaSq, kGnSq
+};
+
+__global__ void k_minres_setup(const double* __restrict__ part, double* sc)
+{
+    const double s = sum_partials_warp(part, kRedBlocks);
+    if (threadIdx.x != 0) return;
+    sc[kGammaSq] = s;
+    const double g = s > 0.0 ? sqrt(s) : 0.0;
+    sc[kGamma] = g;
+    sc[kGammaPrev] = 1.0;
+    sc[kEta] = g;
+    sc[kCPrev] = sc[kC] = 1.0;
+    sc[kSPrev] = sc[kS] = 0.0;
+}
+
+__global__ void k_minres_delta(const double* __restrict__ part, double* sc)
+{
+    const double s = sum_partials_warp(part, kRedBlocks);
+    if (threadIdx.x == 0) sc[kDelta] = s;
+}
+
+__global__ void k_minres_vnext(const double* __restrict__ az, const double* __restrict__ v,
+                               const double* __restrict__ vprev, double* __restrict__ vnext,
+                               const double* __restrict__ sc, int first, long long n)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double c1 = -sc[kDelta] / sc[kGamma];
+    double t = az[i] + c1 * v[i];
+    if (!first) t = t + (-sc[kGamma] / sc[kGammaPrev]) * vprev[i];
+    vnext[i] = t;
+}
+
+__global__ void k_minres_gamma(const double* __restrict__ part, double* sc, int* stop)
+{
+    const double gn_sq = sum_partials_warp(part, kRedBlocks);
+    if (threadIdx.x != 0) return;
+    sc[kGnSq] = gn_sq;
+    if (gn_sq < 0.0) {
+        *stop = 1; // "minres: preconditioner lost definiteness"
+        return;
+    }
+    const double gn = sqrt(gn_sq);
+    sc[kGammaNext] = gn;
+    const double c = sc[kC], cp = sc[kCPrev], s = sc[kS], sp = sc[kSPrev];
+    const double delta = sc[kDelta], gamma = sc[kGamma];
+    const double a0 = c * delta - cp * s * gamma;
+    const double a1 = sqrt(a0 * a0 + gn * gn);
+    const double a2 = s * delta + cp * c * gamma;
+    const double a3 = sp * gamma;
+    sc[kA0] = a0;
+    sc[kA1] = a1;
+    sc[kA2] = a2;
+    sc[kA3] = a3;
+    if (a1 == 0.0) {
+        *stop = 2;
+        return;
+    }
+    sc[kCNext] = a0 / a1;
+    sc[kSNext] = gn / a1;
+}
+
+__global__ void k_minres_update(const double* __restrict__ z, const double* __restrict__ wprev,
+                                const double* __restrict__ w, double* __restrict__ wnext,
+                                double* __restrict__ x, const double* __restrict__ sc,
+                                const int* __restrict__ stop, long long n)
+{
+    if (*stop) return;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double a1 = sc[kA1], a2 = sc[kA2], a3 = sc[kA3];
+    double t = z[i] + (-a3) * wprev[i];
+    t = t + (-a2) * w[i];
+    t = t * (1.0 / a1);
+    wnext[i] = t;
+    x[i] += (sc[kCNext] * sc[kEta]) * t;
+}
+
+__global__ void k_minres_rotate(double* sc, const int* stop)
+{
+    if (*stop) return;
+    sc[kEta] = -sc[kSNext] * sc[kEta];
+    sc[kGammaPrev] = sc[kGamma];
+    sc[kGamma] = sc[kGammaNext];
+    sc[kCPrev] = sc[kC];
+    sc[kC] = sc[kCNext];
+    sc[kSPrev] = sc[kS];
+    sc[kS] = sc[kSNext];
+}
+
+} // namespace
+
+void launch_dot_partials(cudaStream_t s, const double* x, const double* y, long long n,
+                         double* part)
+{
+    k_dot_partials<<<kRedBlocks, kRedThreads, 0, s>>>(x, y, n, part);
+}
+
+void launch_finalize(cudaStream_t s, const double* part, double* dst, int mode)
+{
+    k_finalize<<<1, 32, 0, s>>>(part, dst, mode);
+}
+
+void launch_copy(cudaStream_t s, const double* x, double* y, long long n)
+{
+    if (n > 0) k_copy<<<blocks_for(n), kT, 0, s>>>(x, y, n);
+}
+
+void launch_fill(cudaStream_t s, double* x, double v, long long n)
+{
+    if (n > 0) k_fill<<<blocks_for(n), kT, 0, s>>>(x, v, n);
+}
+
+void launch_scale_inv(cudaStream_t s, const double* x, const double* den, double* y, long long n,
+                      const int* stop)
+{
+    k_scale_inv<<<blocks_for(n), kT, 0, s>>>(x, den, y, n, stop);
+}
+
+void launch_axpy_neg(cudaStream_t s, const double* h, const double* v, double* w, long long n)
+{
+    k_axpy_neg<<<blocks_for(n), kT, 0, s>>>(h, v, w, n);
+}
+
+void launch_combine(cudaStream_t s, const double* const* Ztab, const double* y, int m, double* x,
+                    long long n, const double* xbase)
+{
+    k_combine<<<blocks_for(n), kT, 0, s>>>(Ztab, y, m, x, n, xbase);
+}
+
+void launch_add(cudaStream_t s, const double* a, const double* b, double* out, long long n)
+{
+    k_add<<<blocks_for(n), kT, 0, s>>>(a, b, out, n);
+}
+
+void launch_mgs_step(cudaStream_t s, const double* part, const GmresDev& G, int i, int j,
+                     const double* vi, double* w, long long n)
+{
+    k_mgs_step<<<kRedBlocks * 4, kT, 0, s>>>(part, G.H, G.ld, i, j, vi, w, n);
+}
+
+void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j)
+{
+    k_gmres_givens<<<1, 32, 0, s>>>(part, G, j);
+}
+
+void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst)
+{
+    k_relres<<<1, 32, 0, s>>>(part, bnorm, dst);
+}
+
+void launch_minres_setup(cudaStream_t s, const double* part, double* sc)
+{
+    k_minres_setup<<<1, 32, 0, s>>>(part, sc);
+}
+
+void launch_minres_delta(cudaStream_t s, const double* part, double* sc)
+{
+    k_minres_delta<<<1, 32, 0, s>>>(part, sc);
+}
+
+void launch_minres_vnext(cudaStream_t s, const double* az, const double* v, const double* vprev,
+                         double* vnext, const double* sc, int first, long long n)
+{
+    k_minres_vnext<<<blocks_for(n), kT, 0, s>>>(az, v, vprev, vnext, sc, first, n);
+}
+
+void launch_minres_gamma(cudaStream_t s, const double* part, double* sc, int* stop)
+{
+    k_minres_gamma<<<1, 32, 0, s>>>(part, sc, stop);
+}
+
+void launch_minres_update(cudaStream_t s, const double* z, const double* wprev, const double* w,
+                          double* wnext, double* x, const double* sc, const int* stop,
+                          long long n)
+{
+    k_minres_update<<<blocks_for(n), kT, 0, s>>>(z, wprev, w, wnext, x, sc, stop, n);
+}
+
+void launch_minres_rotate(cudaStream_t s, double* sc, const int* stop)
+{
+    k_minres_rotate<<<1, 1, 0, s>>>(sc, stop);
+}
+
+} // namespace ocb

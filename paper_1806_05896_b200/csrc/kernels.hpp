@@ -1,0 +1,220 @@
+// Host-callable launchers for the sm_100a kernels (FP64, bandwidth-bound).
+// Every launcher enqueues on the given stream and never synchronises.
+#pragma once
+
+#include "oc_common.cuh"
+
+namespace ocb {
+
+// ---------------------------------------------------------------- multigrid
+struct MgLevelDev {
+    Op9 op;          // level operator (fine: constant stencil + diag, coarse: 9 arrays)
+    double* x;       // level iterate (coarse levels only; fine uses caller buffers)
+    double* b;       // level right-hand side (coarse levels only)
+};
+
+constexpr int kBottomMaxLevels = 6;   // levels 2..7 at most in the single-CTA solver
+constexpr int kBottomTopLevel = 6;    // grid levels <= this run inside one CTA
+
+struct BottomArgs {
+    int nlev;                          // number of levels handled (top .. level 2)
+    Op9 ops[kBottomMaxLevels];         // [0] = top level of the bottom solver
+    const double* lu;                  // 9x9 LU of the level-2 matrix (column-major)
+    const int* perm;
+};
+
+// One symmetric-colour Gauss-Seidel sweep (4 colour passes fused via halo
+// recomputation), out of place: x_in -> x_out (must differ). forward: colours
+// 0..3, backward: 3..0. zero_init treats x_in as 0; if ec != nullptr,
+// x += P*ec (bilinear prolongation from the coarse level) is applied on load.
+void launch_gs_sweep(cudaStream_t s, const Op9& A, const double* b, const double* x_in,
+                     double* x_out, bool forward, bool zero_init, const double* ec,
+                     int sweeps_fused = 1);
+// bc = R (b - A x) with R = P^T, restricting to the coarse level (nxc = (nx-1)/2);
+// also zeroes the coarse iterate xc (if non-null).
+void launch_residual_restrict(cudaStream_t s, const Op9& A, const double* b, const double* x,
+                              double* bc, double* xc);
+// x += P ec
+void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x);
+// partial sums of |b - A x|^2 into part[kRedBlocks]
+void launch_residual_norm_partials(cudaStream_t s, const Op9& A, const double* b,
+                                   const double* x, double* part);
+// Divergence check of MgHierarchy::solve (multigrid.cpp:141-157):
+// res = sqrt(sum part); if (res > 10 * state[0]) flag; state[0] = res.
+void launch_mg_check(cudaStream_t s, const double* part, double* state, int* flags);
+// state[0] = ||b||  (initial "previous residual")
+void launch_norm_init(cudaStream_t s, const double* b, long long n, double* part, double* state);
+// Galerkin R A P into 9 coarse arrays; if base != nullptr the result is base + RAP.
+// batch > 1 (heat blocks): fine coef/diag and coarse arrays advance by the given strides.
+// If rem_out != nullptr the bare R A P is also written there (rediscretised chain).
+void launch_rap(cudaStream_t s, const Op9& fine, double* coarse, const double* base,
+                double* rem_out, int batch, long long fine_coef_stride,
+                long long fine_diag_stride, long long coarse_stride);
+// Fine remainder of a rediscretised hierarchy (multigrid.cpp:86-88):
+// rem9 = fine - base over all 9 entries (fine may be constant + diag or arrays).
+void launch_remainder9(cudaStream_t s, const Op9& fine, const double* base9, double* rem9);
+// 9x9 coarse LU with partial pivoting (dense_eig.cpp:87-121 semantics)
+void launch_coarse_lu(cudaStream_t s, const double* coef9, double* lu, int* perm, int batch);
+// whole V-cycle below (and including) the bottom top level in one CTA
+void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double* x, int cycles,
+                   int pre, int post, bool check, double* state, int* flags);
+
+} // namespace ocb
+
+namespace ocb {
+
+// ------------------------------------------------------------- problem ops
+// Device view of the saddle-system blocks (reference ipm.cpp:347-374 for the
+// steady model, timedep.cpp:18-133 for the space-time heat model).
+struct ProbDev {
+    int nx;             // spatial interior nodes per side
+    long long ns;       // spatial nodes per block (nx*nx)
+    int nt;             // time blocks (1 for steady problems)
+    long long ny;       // ns * nt
+    int heat;           // 1 = space-time heat model
+    int has_sb;         // state box present (theta_y, lam_y used)
+    Op9 L;              // constraint operator K (steady): Poisson or SUPG convdiff
+    Op9 LT;             // K^T (steady)
+    Op9 M;              // consistent mass (constant stencil)
+    Op9 Mobs;           // observation mass (M or the partial mass)
+    Op9 Mtl;            // heat: M + tau L (constant stencil)
+    double alpha, beta, tau;
+    const double* qw;   // heat: quadrature weight per time block (device)
+};
+
+// out = A x for the reduced saddle operator (make_saddle_operator,
+// ipm.cpp:237-268); if part != nullptr, instead accumulate |b - A x|^2 block
+// partials (true residual, krylov.cpp:23-34) and optionally still write out.
+void launch_kkt(cudaStream_t s, const ProbDev& P, const double* ty, const double* tw,
+                const double* tv, const double* x, double* out, const double* b, double* part);
+
+// Chebyshev semi-iteration on s_k*M + diag(e) per block (chebyshev.cpp:49-75).
+// e may be null (zero extra diagonal). Writes the result to out[0..ny).
+struct ChebWork {
+    double* g;
+    double* r0;
+    double* r1;
+    double* r2;
+};
+void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const double* e,
+                      int steps, const ChebWork& w, double* out);
+
+// 2x2 control block inverse (precond.cpp:37-53, 148-157; heat timedep.cpp:383-393)
+void launch_control_2x2(cudaStream_t s, const ProbDev& P, const double* tw, const double* tv,
+                        const double* rw, const double* rv, double* vw, double* vv,
+                        int* flags);
+// P_T coupling row: steady t = L vy - M vw + M vv - rp (precond.cpp:223-227);
+// heat t = Ldt vy - tau M (vw - vv) - rp (timedep.cpp:411-418)
+void launch_coupling(cudaStream_t s, const ProbDev& P, const double* vy, const double* vw,
+                     const double* vv, const double* rp, double* t);
+// Schur middle: steady t2 = M_obs t1 + theta_y t1 (precond.cpp:133-134);
+// heat u_k = tau w_k M t_k + theta_y t_k (timedep.cpp:289-296). ty may be null.
+void launch_schur_middle(cudaStream_t s, const ProbDev& P, const double* ty, const double* t1,
+                         double* t2);
+// matching diagonals: steady bracket = d^2 s/(alpha d s + 1) (precond.cpp:55-72),
+// mhat = sqrt(bracket) sqrt(d + theta_y) (precond.cpp:74-84); heat time_m_hat
+// (timedep.cpp:215-243). Either output may be null; ty may be null (zero).
+void launch_mhat(cudaStream_t s, const ProbDev& P, const double* ty, const double* tw,
+                 const double* tv, double* mhat, double* bracket, int* flags);
+// out[i] = a[i] + b[i] over n (9-point coefficient sums, e.g. L^T + M_obs)
+void launch_add(cudaStream_t s, const double* a, const double* b, double* out, long long n);
+// P_Pi pieces (precond.cpp:287-308):
+// rhs1 = M (v2w - v2v) + rp
+void launch_ppi_rhs1(cudaStream_t s, const ProbDev& P, const double* vw, const double* vv,
+                     const double* rp, double* rhs1);
+// t = M_obs v1 + (theta_y v1 - ry)
+void launch_ppi_t(cudaStream_t s, const ProbDev& P, const double* ty, const double* v1,
+                  const double* ry, double* t);
+// y = A x for a single 9-point operator (steady field)
+void launch_op_apply(cudaStream_t s, const Op9& A, const double* x, double* y);
+// heat: out_k = M x_{k-1} added (forward) or M x_{k+1} (backward) into rhs_k:
+// rhs = r_k + M x_nb  (timedep.cpp:277-286, 300-309)
+void launch_rhs_plus_mass(cudaStream_t s, const ProbDev& P, const double* r, const double* xnb,
+                          double* rhs);
+
+// --------------------------------------------------------------- vectors
+void launch_dot_partials(cudaStream_t s, const double* x, const double* y, long long n,
+                         double* part);
+// dst = op(sum partials): mode 0 sum, 1 sqrt(sum)
+void launch_finalize(cudaStream_t s, const double* part, double* dst, int mode);
+void launch_copy(cudaStream_t s, const double* x, double* y, long long n);
+void launch_fill(cudaStream_t s, double* x, double v, long long n);
+// y = x * (1/ *den)     (scaled(1.0/den, x))
+void launch_scale_inv(cudaStream_t s, const double* x, const double* den, double* y, long long n,
+                      const int* stop);
+// w += (-(*h)) * v      (axpy(-h, v, w))
+void launch_axpy_neg(cudaStream_t s, const double* h, const double* v, double* w, long long n);
+// x = sum_i y[i] * Z_i with Z_i = Ztab[i] (device pointer table), the GMRES
+// iterate rebuild (krylov.cpp:196-197)
+// If xbase != nullptr: x = xbase + sum (restarted GMRES).
+void launch_combine(cudaStream_t s, const double* const* Ztab, const double* y, int m, double* x,
+                    long long n, const double* xbase = nullptr);
+
+// ----------------------------------------------------------------- GMRES
+// Device state of one GMRES solve (krylov.cpp:133-212); H column-major
+// (ld = maxit+1), cs/sn/g rotations, y the current LS solution.
+struct GmresDev {
+    double* H;      // (maxit+1) x maxit
+    double* cs;
+    double* sn;
+    double* g;      // maxit+1
+    double* y;      // maxit
+    double* scal;   // [0] bnorm, [1] hnext, [2] relres, [3] h_i scratch
+    int* stop;      // 0 running, 1 zero pivot
+    int ld;
+};
+// h_i = <w, V_i> from partials, stored at H(i, j); then w -= h_i V_i
+void launch_mgs_step(cudaStream_t s, const double* part, const GmresDev& G, int i, int j,
+                     const double* vi, double* w, long long n);
+// hnext from partials -> H(j+1, j), Givens update and back substitution for y (one thread)
+void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j);
+// scal[2] = sqrt(sum part) / bnorm
+void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst);
+
+// ----------------------------------------------------------------- MINRES
+// scalar state (krylov.cpp:37-131): see k_vec.cu for the slot layout
+void launch_minres_setup(cudaStream_t s, const double* part, double* sc);
+void launch_minres_delta(cudaStream_t s, const double* part, double* sc);
+void launch_minres_vnext(cudaStream_t s, const double* az, const double* v, const double* vprev,
+                         double* vnext, const double* sc, int first, long long n);
+void launch_minres_gamma(cudaStream_t s, const double* part, double* sc, int* stop);
+void launch_minres_update(cudaStream_t s, const double* z, const double* wprev, const double* w,
+                          double* wnext, double* x, const double* sc, const int* stop,
+                          long long n);
+void launch_minres_rotate(cudaStream_t s, double* sc, const int* stop);
+
+
+// ------------------------------------------------------------------- IPM
+// Device state of the interior point iteration (ipm.hpp:36-42) and the
+// problem vectors of the model (ipm.hpp:83-88).
+struct IpmDev {
+    double *y, *z, *p, *lya, *lyb, *lza, *lzb;
+    const double *yd, *f, *za, *zb, *ya, *yb, *ld;
+    double *ty, *tw, *tv;
+    double *dy, *dz, *dp, *dlya, *dlyb, *dlza, *dlzb;
+};
+// build_theta (ipm.cpp:32-61)
+void launch_theta(cudaStream_t s, const ProbDev& P, const IpmDev& S, int* flags);
+// newton_rhs (ipm.cpp:112-143) into rhs = [r1 | r2 | r3]
+void launch_newton_rhs(cudaStream_t s, const ProbDev& P, const IpmDev& S, double mu, double* rhs);
+// recover_multiplier_steps + ratio partials (ipm.cpp:145-210); part: 2*kRedBlocks mins
+void launch_recover_ratios(cudaStream_t s, const ProbDev& P, const IpmDev& S, double mu,
+                           double* part);
+// alpha_P, alpha_D = min(1, alpha0 * ratio) -> steps[0..1]
+void launch_step_lengths(cudaStream_t s, const double* part, double alpha0, double* steps);
+// state update + interiority checks (ipm.cpp:305-319)
+void launch_ipm_update(cudaStream_t s, const ProbDev& P, const IpmDev& S, const double* steps,
+                       int* flags);
+// ipm_residuals squared sums (ipm.cpp:63-110): part 3*kRedBlocks -> norms[0..2] (RMS)
+void launch_ipm_residuals(cudaStream_t s, const ProbDev& P, const IpmDev& S, double mu,
+                          double* part, double* norms);
+// objective (qp.cpp:112-121 / heat closures) and sparsity of u = w - v
+// out: [0] J, [1] count |u|<thr, [2] l1
+void launch_objective(cudaStream_t s, const ProbDev& P, const IpmDev& S, double* part,
+                      double* out);
+// initial_point (ipm.cpp:212-235)
+void launch_initial_point(cudaStream_t s, const ProbDev& P, const IpmDev& S);
+// u = w - v
+void launch_recover_control(cudaStream_t s, long long ny, const double* z, double* u);
+
+} // namespace ocb

@@ -1,0 +1,1168 @@
+// Host orchestration of the device-resident IPM Newton solve (see solver.hpp).
+//
+// Reference call structure reproduced here:
+//   ipm_solve                      ipm.cpp:270-341
+//   make_steady_model/newton_solve ipm.cpp:388-470
+//   make_spacetime_model           timedep.cpp:313-441
+//   Block11Approx/SchurApprox/...  precond.cpp:110-308
+//   MgHierarchy build/solve        multigrid.cpp:75-157
+//   minres / gmres                 krylov.cpp:37-212
+#include "solver.hpp"
+
+#include "assembly.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace ocb {
+
+void cuda_check(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static void launch_check(const char* what) { cuda_check(cudaGetLastError(), what); }
+
+Ctx::Ctx(int dev) : device(dev)
+{
+    int count = 0;
+    cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (dev < 0 || dev >= count) throw CudaFailure("oc_create: no such CUDA device");
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreate(&ev0), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
+    cuda_check(cudaMallocHost(&hscal, 64 * sizeof(double)), "cudaMallocHost");
+    cuda_check(cudaMallocHost(&hflags, 8 * sizeof(int)), "cudaMallocHost");
+}
+
+Ctx::~Ctx()
+{
+    if (stream) cudaStreamSynchronize(stream);
+    if (hscal) cudaFreeHost(hscal);
+    if (hflags) cudaFreeHost(hflags);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void Ctx::sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+
+bool is_device_ptr(const void* p)
+{
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void copy_any(Ctx& c, void* dst, const void* src, size_t bytes)
+{
+    if (!bytes) return;
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c.stream), "cudaMemcpyAsync");
+}
+
+// =================================================================== Hierarchy
+void Hierarchy::allocate(int level, int batch)
+{
+    if (level < 3) throw InvalidArgument("MgHierarchy: fine level must be >= 3");
+    if (built_ && level == level_ && batch == batch_) return;
+    level_ = level;
+    batch_ = batch;
+    K_ = level - 2;
+    nx_.assign(K_ + 1, 0);
+    for (int k = 0; k <= K_; ++k) nx_[k] = (1 << (level - k)) - 1;
+    kb_ = 0;
+    while (level - kb_ > kBottomTopLevel) ++kb_;
+    coef_.clear();
+    coef_.resize(K_ + 1);
+    xa_.clear();
+    xb_.clear();
+    b_.clear();
+    xa_.resize(K_ + 1);
+    xb_.resize(K_ + 1);
+    b_.resize(K_ + 1);
+    for (int k = 1; k <= K_; ++k) {
+        const size_t n = (size_t)level_n(k);
+        coef_[k].resize(9 * n * batch);
+        xa_[k].resize(n);
+        xb_[k].resize(n);
+        b_[k].resize(n);
+    }
+    xb_[0].resize((size_t)level_n(0));
+    lu_.resize(81 * (size_t)batch);
+    perm_.resize(9 * (size_t)batch);
+    part_.resize(kRedBlocks);
+    state_.resize(2);
+    built_ = true;
+}
+
+Op9 Hierarchy::level_op(int k, int bt) const
+{
+    if (k == 0) {
+        Op9 a = fine_;
+        if (a.coef) a.coef += bt * fine_coef_stride_;
+        if (a.diag) a.diag += bt * fine_diag_stride_;
+        return a;
+    }
+    Op9 a{};
+    a.nx = nx_[k];
+    a.coef = coef_[k].get() + (size_t)bt * 9 * level_n(k);
+    a.diag = nullptr;
+    a.cscale = 1.0;
+    return a;
+}
+
+void Hierarchy::build(Ctx& c, const Op9& fine, long long fcs, long long fds)
+{
+    fine_ = fine;
+    fine_coef_stride_ = fcs;
+    fine_diag_stride_ = fds;
+    for (int k = 0; k < K_; ++k) {
+        const Op9 f = level_op(k, 0);
+        const long long cs = k == 0 ? fcs : 9 * level_n(k);
+        const long long ds = k == 0 ? fds : 0;
+        launch_rap(c.stream, f, coef_[k + 1].get(), nullptr, nullptr, batch_, cs, ds,
+                   9 * level_n(k + 1));
+    }
+    launch_coarse_lu(c.stream, coef_[K_].get(), lu_.get(), perm_.get(), batch_);
+    launch_check("multigrid build");
+}
+
+void Hierarchy::build_rediscretized(Ctx& c, const Op9& fine, const std::vector<const double*>& base)
+{
+    if (batch_ != 1) throw InvalidArgument("rediscretised hierarchies are not batched");
+    fine_ = fine;
+    fine_coef_stride_ = fine_diag_stride_ = 0;
+    if (rem_.size() != (size_t)K_ + 1) {
+        rem_.clear();
+        rem_.resize(K_ + 1);
+        for (int k = 1; k <= K_; ++k) rem_[k].resize(9 * (size_t)level_n(k));
+        remfine_.resize(9 * (size_t)level_n(0));
+    }
+    // remainder = A_f - base(level_f); coarse = base(l-1) + R remainder P
+    launch_remainder9(c.stream, fine, base[0], remfine_.get());
+    Op9 rem{};
+    rem.nx = nx_[0];
+    rem.coef = remfine_.get();
+    rem.cscale = 1.0;
+    for (int k = 0; k < K_; ++k) {
+        launch_rap(c.stream, rem, coef_[k + 1].get(), base[k + 1], rem_[k + 1].get(), 1, 0, 0,
+                   9 * level_n(k + 1));
+        rem.nx = nx_[k + 1];
+        rem.coef = rem_[k + 1].get();
+    }
+    launch_coarse_lu(c.stream, coef_[K_].get(), lu_.get(), perm_.get(), 1);
+    launch_check("multigrid build (rediscretised)");
+}
+
+BottomArgs Hierarchy::bottom_args(int kfrom, int bt) const
+{
+    BottomArgs a{};
+    a.nlev = K_ - kfrom + 1;
+    if (a.nlev > kBottomMaxLevels) throw RuntimeError("bottom solver: too many levels");
+    for (int j = 0; j < a.nlev; ++j) a.ops[j] = level_op(kfrom + j, bt);
+    a.lu = lu_.get() + 81 * (size_t)bt;
+    a.perm = perm_.get() + 9 * (size_t)bt;
+    return a;
+}
+
+void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_in,
+                       const MgParams& p, int bt, int* flags)
+{
+    if (k == kb_) {
+        launch_bottom(c.stream, bottom_args(kb_, bt), b, xout, 1, p.pre, p.post, false, nullptr,
+                      flags);
+        return;
+    }
+    const Op9 A = level_op(k, bt);
+    double* Abuf = xout;
+    double* Bbuf = xb_[k].get();
+    const int S = p.pre + p.post;
+    auto outbuf = [&](int s) { return ((S - s) % 2 == 0) ? Abuf : Bbuf; };
+    const double* cur = zero_in ? nullptr : xout;
+    const long long n = level_n(k);
+    if (!zero_in && S % 2 == 1) {
+        launch_copy(c.stream, xout, Bbuf, n);
+        cur = Bbuf;
+    }
+    int s = 0;
+    for (int i = 0; i < p.pre; ++i) {
+        ++s;
+        double* out = outbuf(s);
+        launch_gs_sweep(c.stream, A, b, cur, out, true, cur == nullptr, nullptr);
+        cur = out;
+    }
+    if (!cur) {
+        double* out = outbuf(s);
+        launch_fill(c.stream, out, 0.0, n);
+        cur = out;
+    }
+    launch_residual_restrict(c.stream, A, b, cur, b_[k + 1].get(), xa_[k + 1].get());
+    vcycle(c, k + 1, b_[k + 1].get(), xa_[k + 1].get(), true, p, bt, flags);
+    const double* ec = xa_[k + 1].get();
+    if (p.post == 0) {
+        launch_prolong_add(c.stream, nx_[k], ec, const_cast<double*>(cur));
+        return;
+    }
+    for (int i = 0; i < p.post; ++i) {
+        ++s;
+        double* out = outbuf(s);
+        launch_gs_sweep(c.stream, A, b, cur, out, false, false, i == 0 ? ec : nullptr);
+        cur = out;
+    }
+}
+
+void Hierarchy::solve(Ctx& c, const double* b, double* x, const MgParams& p, int bt, int* flags)
+{
+    const long long n = level_n(0);
+    if (kb_ == 0) {
+        launch_bottom(c.stream, bottom_args(0, bt), b, x, p.cycles, p.pre, p.post, true,
+                      state_.get(), flags);
+        launch_check("multigrid bottom solve");
+        return;
+    }
+    if (p.cycles <= 0) {
+        launch_fill(c.stream, x, 0.0, n);
+        return;
+    }
+    launch_norm_init(c.stream, b, n, part_.get(), state_.get());
+    const Op9 A = level_op(0, bt);
+    for (int cyc = 0; cyc < p.cycles; ++cyc) {
+        vcycle(c, 0, b, x, cyc == 0, p, bt, flags);
+        launch_residual_norm_partials(c.stream, A, b, x, part_.get());
+        launch_mg_check(c.stream, part_.get(), state_.get(), flags);
+    }
+    launch_check("multigrid solve");
+}
+
+void Hierarchy::smooth(Ctx& c, const double* b, double* x, bool forward, int bt)
+{
+    const Op9 A = level_op(0, bt);
+    launch_gs_sweep(c.stream, A, b, x, xb_[0].get(), forward, false, nullptr);
+    launch_copy(c.stream, xb_[0].get(), x, level_n(0));
+    launch_check("smoothing sweep");
+}
+
+// ===================================================================== Problem
+namespace {
+
+Op9 const_op(int nx, const double c9[9])
+{
+    Op9 a{};
+    a.nx = nx;
+    a.coef = nullptr;
+    for (int d = 0; d < 9; ++d) a.c[d] = c9[d];
+    a.diag = nullptr;
+    a.cscale = 1.0;
+    return a;
+}
+
+Op9 var_op(int nx, const double* coef)
+{
+    Op9 a{};
+    a.nx = nx;
+    a.coef = coef;
+    a.diag = nullptr;
+    a.cscale = 1.0;
+    return a;
+}
+
+} // namespace
+
+void Problem::upload(DVec& dst, const double* src, size_t n)
+{
+    dst.resize(n);
+    copy_any(ctx, dst.get(), src, n * sizeof(double));
+}
+
+Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
+{
+    if (d.level < 1 || d.level > 14) throw InvalidArgument("Grid: level out of range");
+    if (d.pde < 0 || d.pde > 2) throw InvalidArgument("oc_problem_create: unknown pde");
+    // ControlProblem::validate (qp.cpp:10-28)
+    if (d.alpha <= 0.0) throw InvalidArgument("ControlProblem: alpha must be positive");
+    if (d.beta < 0.0) throw InvalidArgument("ControlProblem: beta must be nonnegative");
+    if (!d.u_a || !d.u_b || !d.y_d) throw InvalidArgument("oc_problem_create: missing data");
+    if ((d.y_a == nullptr) != (d.y_b == nullptr))
+        throw InvalidArgument("ControlProblem: state bounds must come as a pair");
+    level_ = d.level;
+    nx_ = level_nx(level_);
+    ns_ = (long long)nx_ * nx_;
+    heat_ = d.pde == OC_PDE_HEAT;
+    convdiff_ = d.pde == OC_PDE_CONVDIFF;
+    eps_ = d.eps;
+    has_sb_ = d.y_a != nullptr;
+    partial_obs_ = d.has_obs != 0;
+
+    auto host_vec = [&](const double* p, size_t n) {
+        std::vector<double> v(n);
+        if (is_device_ptr(p)) cuda_check(cudaMemcpy(v.data(), p, n * sizeof(double), cudaMemcpyDeviceToHost), "copy");
+        else std::memcpy(v.data(), p, n * sizeof(double));
+        return v;
+    };
+    const std::vector<double> ua = host_vec(d.u_a, ns_), ub = host_vec(d.u_b, ns_);
+    for (long long i = 0; i < ns_; ++i)
+        if (ua[i] > 0.0 || ub[i] < 0.0)
+            throw InvalidArgument("ControlProblem: control bounds must satisfy u_a <= 0 <= u_b");
+    std::vector<double> yah, ybh;
+    if (has_sb_) {
+        yah = host_vec(d.y_a, ns_);
+        ybh = host_vec(d.y_b, ns_);
+        for (long long i = 0; i < ns_; ++i)
+            if (yah[i] > 0.0 || ybh[i] < 0.0)
+                throw InvalidArgument("ControlProblem: state bounds must satisfy y_a <= 0 <= y_b");
+    }
+    if (partial_obs_) {
+        if (d.obs[0] > d.obs[1] || d.obs[2] > d.obs[3])
+            throw InvalidArgument("ObservationRegion: empty box");
+        if (d.obs[1] < 0.0 || d.obs[0] > 1.0 || d.obs[3] < 0.0 || d.obs[2] > 1.0)
+            throw InvalidArgument("ObservationRegion: box outside domain");
+    }
+    if (convdiff_ && d.eps <= 0.0) throw InvalidArgument("assemble_convdiff: eps must be positive");
+
+    nt_ = 1;
+    std::vector<double> qw(1, 1.0);
+    if (heat_) {
+        if (has_sb_) throw InvalidArgument("assemble_spacetime: state bounds not supported in time");
+        if (partial_obs_)
+            throw InvalidArgument("assemble_spacetime: partial observation not supported in time");
+        if (d.tau <= 0.0) throw InvalidArgument("assemble_spacetime: tau must be positive");
+        const double steps = d.horizon / d.tau;
+        const long nt = std::lround(steps);
+        if (nt < 1 || std::abs(steps - (double)nt) > 1e-9)
+            throw InvalidArgument("assemble_spacetime: tau must divide the horizon");
+        nt_ = (int)nt;
+        qw.assign(nt_, 1.0);
+        if (d.quadrature == 1) {
+            qw.front() = 0.5;
+            qw.back() = 0.5;
+        }
+    }
+    ny_ = ns_ * nt_;
+    if (heat_) {
+        if (d.y_d_len != ns_ && d.y_d_len != ny_)
+            throw InvalidArgument("assemble_spacetime: nodal data size mismatch");
+    } else if (d.y_d_len != ns_) {
+        throw InvalidArgument("build_qp: nodal data size mismatch with grid");
+    }
+
+    // ---- operators (fem.cpp assembly restated in assembly.cpp)
+    const std::vector<double> M9 = assemble_mass9(level_);
+    double cM[9];
+    if (!constant_stencil(M9, level_, cM) && nx_ >= 3)
+        throw RuntimeError("internal: mass stencil is not grid-constant");
+    if (nx_ < 3) for (int k = 0; k < 9; ++k) cM[k] = M9[k * ns_ + (ns_ / 2)];
+    P = ProbDev{};
+    P.nx = nx_;
+    P.ns = ns_;
+    P.nt = nt_;
+    P.ny = ny_;
+    P.heat = heat_ ? 1 : 0;
+    P.has_sb = has_sb_ ? 1 : 0;
+    P.alpha = d.alpha;
+    P.beta = d.beta;
+    P.tau = heat_ ? d.tau : 0.0;
+    P.M = const_op(nx_, cM);
+    P.Mobs = P.M;
+    if (convdiff_) {
+        const std::vector<double> L9 = assemble_convdiff9(level_, d.eps, true);
+        const std::vector<double> LT9 = transpose9(L9, level_);
+        upload(Lc_, L9.data(), L9.size());
+        upload(LTc_, LT9.data(), LT9.size());
+        P.L = var_op(nx_, Lc_.get());
+        P.LT = var_op(nx_, LTc_.get());
+        // per-level SUPG bases for the rediscretised hierarchies (qp.cpp:143-145)
+        base_.clear();
+        baseT_.clear();
+        base_.resize(level_ - 1);
+        baseT_.resize(level_ - 1);
+        for (int k = 0; k + 2 <= level_; ++k) {
+            const int l = level_ - k;
+            const std::vector<double> b9 = k == 0 ? L9 : assemble_convdiff9(l, d.eps, true);
+            const std::vector<double> bt9 = transpose9(b9, l);
+            upload(base_[k], b9.data(), b9.size());
+            upload(baseT_[k], bt9.data(), bt9.size());
+        }
+    } else {
+        const std::vector<double> L9 = assemble_poisson9(level_);
+        double cL[9];
+        if (!constant_stencil(L9, level_, cL))
+            for (int k = 0; k < 9; ++k) cL[k] = L9[k * ns_ + ns_ / 2];
+        P.L = const_op(nx_, cL);
+        P.LT = P.L;
+        if (heat_) {
+            // Mtl = sparse_add(1, M, 1, tau L) (timedep.cpp:150-153)
+            double cMtl[9];
+            for (int k = 0; k < 9; ++k) cMtl[k] = 1.0 * cM[k] + 1.0 * (cL[k] * d.tau);
+            P.Mtl = const_op(nx_, cMtl);
+        }
+    }
+    if (partial_obs_) {
+        const std::vector<double> Mo9 = assemble_partial_mass9(level_, d.obs);
+        upload(Mobsc_, Mo9.data(), Mo9.size());
+        P.Mobs = var_op(nx_, Mobsc_.get());
+    }
+
+    // ---- problem vectors (build_qp qp.cpp:123-174, assemble_spacetime timedep.cpp:166-213)
+    const std::vector<double> ld = lumped_diag(level_);
+    upload(ld_, ld.data(), ld.size());
+    std::vector<double> fn(ns_, 0.0);
+    if (d.f) fn = host_vec(d.f, ns_);
+    std::vector<double> mf(ns_, 0.0);
+    for (long long i = 0; i < ns_; ++i) {
+        const int gx = (int)(i % nx_), gy = (int)(i / nx_);
+        double s = 0.0;
+        for (int k = 0; k < 9; ++k) {
+            const int jx = gx + k % 3 - 1, jy = gy + k / 3 - 1;
+            if (jx < 0 || jx >= nx_ || jy < 0 || jy >= nx_) continue;
+            s += M9[k * ns_ + i] * fn[(long long)jy * nx_ + jx];
+        }
+        mf[i] = s;
+    }
+    std::vector<double> fh(ny_);
+    for (int k = 0; k < nt_; ++k)
+        for (long long i = 0; i < ns_; ++i) fh[k * ns_ + i] = heat_ ? d.tau * mf[i] : mf[i];
+    upload(f_, fh.data(), fh.size());
+    // split bounds (qp.cpp:31-44) with the pinned-bound inflation (qp.cpp:162-166)
+    std::vector<double> za(2 * ns_), zb(2 * ns_);
+    for (long long i = 0; i < ns_; ++i) {
+        if (ua[i] > ub[i]) throw InvalidArgument("split_bounds: u_a > u_b");
+        za[i] = std::max(ua[i], 0.0);
+        za[ns_ + i] = -std::min(ub[i], 0.0);
+        zb[i] = std::max(ub[i], 0.0);
+        zb[ns_ + i] = -std::min(ua[i], 0.0);
+    }
+    for (size_t i = 0; i < za.size(); ++i)
+        if (zb[i] - za[i] < 1e-12) zb[i] = za[i] + 1e-12;
+    std::vector<double> zah(2 * ny_), zbh(2 * ny_);
+    for (int k = 0; k < nt_; ++k)
+        for (long long i = 0; i < ns_; ++i) {
+            zah[k * ns_ + i] = za[i];
+            zah[ny_ + k * ns_ + i] = za[ns_ + i];
+            zbh[k * ns_ + i] = zb[i];
+            zbh[ny_ + k * ns_ + i] = zb[ns_ + i];
+        }
+    upload(za_, zah.data(), zah.size());
+    upload(zb_, zbh.data(), zbh.size());
+    if (has_sb_) {
+        upload(ya_, yah.data(), yah.size());
+        upload(yb_, ybh.data(), ybh.size());
+    }
+    {
+        std::vector<double> ydh(ny_);
+        const std::vector<double> src = host_vec(d.y_d, (size_t)d.y_d_len);
+        for (long long g = 0; g < ny_; ++g) ydh[g] = (d.y_d_len == ny_) ? src[g] : src[g % ns_];
+        upload(yd_, ydh.data(), ydh.size());
+    }
+    upload(qw_, qw.data(), qw.size());
+    P.qw = qw_.get();
+
+    // ---- state, work and scalars
+    const size_t N = (size_t)ny_;
+    y_.resize(N); z_.resize(2 * N); p_.resize(N);
+    lza_.resize(2 * N); lzb_.resize(2 * N); dlza_.resize(2 * N); dlzb_.resize(2 * N);
+    if (has_sb_) { lya_.resize(N); lyb_.resize(N); dlya_.resize(N); dlyb_.resize(N); }
+    ty_.resize(N); tw_.resize(N); tv_.resize(N);
+    rhs_.resize(4 * N); sol_.resize(4 * N);
+    mhat_.resize(N); bracket_.resize(N);
+    cg_.resize(N); c0_.resize(N); c1_.resize(N); c2_.resize(N);
+    t_.resize(N); t2_.resize(N); t3_.resize(N);
+    if (heat_) { tf_.resize(N); rblk_.resize((size_t)ns_); }
+    part_.resize(8 * kRedBlocks);
+    scal_.resize(64);
+    flags_.resize(4);
+    stop_.resize(2);
+    cuda_check(cudaMemsetAsync(flags_.get(), 0, 4 * sizeof(int), ctx.stream), "memset");
+    cuda_check(cudaMemsetAsync(stop_.get(), 0, 2 * sizeof(int), ctx.stream), "memset");
+    launch_fill(ctx.stream, ty_.get(), 0.0, (long long)N);
+
+    S = IpmDev{};
+    S.y = y_.get(); S.z = z_.get(); S.p = p_.get();
+    S.lya = lya_.get(); S.lyb = lyb_.get(); S.lza = lza_.get(); S.lzb = lzb_.get();
+    S.yd = yd_.get(); S.f = f_.get(); S.za = za_.get(); S.zb = zb_.get();
+    S.ya = ya_.get(); S.yb = yb_.get(); S.ld = ld_.get();
+    S.ty = ty_.get(); S.tw = tw_.get(); S.tv = tv_.get();
+    S.dy = sol_.get(); S.dz = sol_.get() + N; S.dp = sol_.get() + 3 * N;
+    S.dlya = dlya_.get(); S.dlyb = dlyb_.get(); S.dlza = dlza_.get(); S.dlzb = dlzb_.get();
+    launch_check("problem setup");
+    ctx.sync();
+}
+
+oc_problem_info Problem::info() const
+{
+    oc_problem_info i{};
+    i.n = (int)ns_;
+    i.nt = nt_;
+    i.ny = ny_;
+    i.kkt_dim = 4 * ny_;
+    i.has_state_bounds = has_sb_;
+    i.partial_observation = partial_obs_;
+    i.symmetric_k = convdiff_ ? 0 : 1;
+    i.level = level_;
+    return i;
+}
+
+void Problem::check_flags(bool sync_now)
+{
+    if (sync_now) {
+        cuda_check(cudaMemcpyAsync(ctx.hflags, flags_.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx.stream),
+                   "flags readback");
+        ctx.sync();
+    }
+    const int f = ctx.hflags[0];
+    if (!f) return;
+    cudaMemsetAsync(flags_.get(), 0, sizeof(int), ctx.stream);
+    if (f & kErrThetaZ) throw RuntimeError("build_theta: lost interiority in z");
+    if (f & kErrThetaY) throw RuntimeError("build_theta: lost interiority in y");
+    if (f & kErrBadInput) throw InvalidArgument("matching_bracket: inputs must be positive");
+    if (f & kErrNegBracket)
+        throw RuntimeError(heat_ ? "time_m_hat: negative bracket"
+                                 : "matching_bracket: negative bracket entry");
+    if (f & kErrSingular2x2) throw RuntimeError("block_2x2_inverse_apply: singular pivot block");
+    if (f & kErrMgDiverged)
+        throw RuntimeError("MgHierarchy::solve: residual growth, cycle diverged");
+    if (f & kErrYInterior) throw RuntimeError("ipm: lost strict interiority in y");
+    if (f & kErrLamYa) throw RuntimeError("ipm: multiplier not positive in lam_ya");
+    if (f & kErrLamYb) throw RuntimeError("ipm: multiplier not positive in lam_yb");
+    if (f & kErrZInterior) throw RuntimeError("ipm: lost strict interiority in z");
+    if (f & kErrLamZa) throw RuntimeError("ipm: multiplier not positive in lam_za");
+    if (f & kErrLamZb) throw RuntimeError("ipm: multiplier not positive in lam_zb");
+    throw RuntimeError("device error flag " + std::to_string(f));
+}
+
+double Problem::read_scalar(const double* dptr)
+{
+    cuda_check(cudaMemcpyAsync(ctx.hscal, dptr, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream),
+               "scalar readback");
+    ctx.sync();
+    return ctx.hscal[0];
+}
+
+void Problem::set_theta(const double* ty, const double* tw, const double* tv)
+{
+    if (ty) copy_any(ctx, ty_.get(), ty, ny_ * sizeof(double));
+    else launch_fill(ctx.stream, ty_.get(), 0.0, ny_);
+    copy_any(ctx, tw_.get(), tw, ny_ * sizeof(double));
+    copy_any(ctx, tv_.get(), tv, ny_ * sizeof(double));
+}
+
+void Problem::kkt(const double* x, double* out)
+{
+    launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(), x, out,
+               nullptr, nullptr);
+}
+
+void Problem::setup_precond(int kind, const oc_ipm_params& p)
+{
+    if (p.cheb_steps < 1) throw InvalidArgument("chebyshev: steps must be >= 1");
+    mg_.cycles = p.mg_cycles;
+    mg_.pre = p.mg_pre;
+    mg_.post = p.mg_post;
+    cheb_steps_ = p.cheb_steps;
+    int* fl = flags_.get();
+    const double* ty = has_sb_ ? ty_.get() : nullptr;
+    if (heat_) {
+        // TimeSchurApprox (timedep.cpp:245-261): one hierarchy per time block on
+        // M + tau L + diag(mhat_k), built as a batch
+        launch_mhat(ctx.stream, P, nullptr, tw_.get(), tv_.get(), mhat_.get(), nullptr, fl);
+        Hheat_.allocate(level_, nt_);
+        Op9 f = P.Mtl;
+        f.diag = mhat_.get();
+        Hheat_.build(ctx, f, 0, ns_);
+    } else if (kind == OC_PRECOND_PPI) {
+        // PermutedPrecond (precond.cpp:262-285)
+        launch_mhat(ctx.stream, P, nullptr, tw_.get(), tv_.get(), nullptr, bracket_.get(), fl);
+        if (!HL_built_) {
+            HL_.allocate(level_);
+            if (convdiff_) {
+                std::vector<const double*> b;
+                for (auto& v : base_) b.push_back(v.get());
+                HL_.build_rediscretized(ctx, P.L, b);
+            } else {
+                HL_.build(ctx, P.L);
+            }
+            HL_built_ = true;
+        }
+        if (!LTpMobs_) {
+            // left = L^T + M_obs (+ diag theta_y), sparse_add (precond.cpp:238)
+            std::vector<double> LT9 = convdiff_ ? transpose9(assemble_convdiff9(level_, eps_, true), level_)
+                                                : assemble_poisson9(level_);
+            std::vector<double> Mo9;
+            if (partial_obs_) {
+                Mo9.resize(9 * (size_t)ns_);
+                cuda_check(cudaMemcpy(Mo9.data(), Mobsc_.get(), Mo9.size() * sizeof(double),
+                                      cudaMemcpyDeviceToHost), "copy");
+            } else {
+                Mo9 = assemble_mass9(level_);
+            }
+            for (size_t i = 0; i < LT9.size(); ++i) LT9[i] = 1.0 * LT9[i] + 1.0 * Mo9[i];
+            upload(LTpMobs_, LT9.data(), LT9.size());
+        }
+        Op9 left = var_op(nx_, LTpMobs_.get());
+        left.diag = ty;
+        Op9 right = P.L;
+        right.diag = bracket_.get();
+        Hleft_.allocate(level_);
+        Hright_.allocate(level_);
+        if (convdiff_) {
+            std::vector<const double*> b, bt;
+            for (auto& v : base_) b.push_back(v.get());
+            for (auto& v : baseT_) bt.push_back(v.get());
+            Hleft_.build_rediscretized(ctx, left, bt);
+            Hright_.build_rediscretized(ctx, right, b);
+        } else {
+            Hleft_.build(ctx, left);
+            Hright_.build(ctx, right);
+        }
+    } else {
+        // Block11Approx + SchurApprox (precond.cpp:110-169): F = L + diag(mhat)
+        launch_mhat(ctx.stream, P, ty, tw_.get(), tv_.get(), mhat_.get(), nullptr, fl);
+        Op9 F = P.L;
+        F.diag = mhat_.get();
+        HF_.allocate(level_);
+        if (convdiff_) {
+            std::vector<const double*> b, bt;
+            for (auto& v : base_) b.push_back(v.get());
+            for (auto& v : baseT_) bt.push_back(v.get());
+            HF_.build_rediscretized(ctx, F, b);
+            Op9 FT = P.LT;
+            FT.diag = mhat_.get();
+            HFT_.allocate(level_);
+            HFT_.build_rediscretized(ctx, FT, bt);
+        } else {
+            HF_.build(ctx, F);
+        }
+    }
+    setup_kind_ = kind;
+    launch_check("preconditioner setup");
+}
+
+void Problem::schur_apply(const double* r, double* out)
+{
+    if (heat_) {
+        time_schur(r, out);
+        return;
+    }
+    // SchurApprox::apply_inverse (precond.cpp:130-136)
+    int* fl = flags_.get();
+    HF_.solve(ctx, r, t2_.get(), mg_, 0, fl);
+    launch_schur_middle(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, t2_.get(), t3_.get());
+    (convdiff_ ? HFT_ : HF_).solve(ctx, t3_.get(), out, mg_, 0, fl);
+}
+
+void Problem::time_schur(const double* r, double* out)
+{
+    // TimeSchurApprox::apply_inverse (timedep.cpp:268-311)
+    int* fl = flags_.get();
+    for (int k = 0; k < nt_; ++k) {
+        const long long off = (long long)k * ns_;
+        launch_rhs_plus_mass(ctx.stream, P, r + off, k > 0 ? tf_.get() + off - ns_ : nullptr,
+                             rblk_.get());
+        Hheat_.solve(ctx, rblk_.get(), tf_.get() + off, mg_, k, fl);
+    }
+    launch_schur_middle(ctx.stream, P, nullptr, tf_.get(), t3_.get());
+    for (int k = nt_ - 1; k >= 0; --k) {
+        const long long off = (long long)k * ns_;
+        launch_rhs_plus_mass(ctx.stream, P, t3_.get() + off,
+                             k + 1 < nt_ ? out + off + ns_ : nullptr, rblk_.get());
+        Hheat_.solve(ctx, rblk_.get(), out + off, mg_, k, fl);
+    }
+}
+
+void Problem::precond_apply(int kind, const double* r, double* out)
+{
+    if (setup_kind_ < 0) throw InvalidArgument("preconditioner not set up");
+    const long long N = ny_;
+    const double* ry = r;
+    const double* rw = r + N;
+    const double* rv = r + 2 * N;
+    const double* rp = r + 3 * N;
+    double* oy = out;
+    double* ow = out + N;
+    double* ov = out + 2 * N;
+    double* op = out + 3 * N;
+    int* fl = flags_.get();
+    const double* ty = has_sb_ ? ty_.get() : nullptr;
+    if (kind == OC_PRECOND_PPI) {
+        if (heat_) throw InvalidArgument("gmres-ppi is not available for heat problems");
+        if (setup_kind_ != OC_PRECOND_PPI) throw InvalidArgument("P_Pi not set up");
+        // PermutedPrecond::apply (precond.cpp:287-308)
+        launch_control_2x2(ctx.stream, P, tw_.get(), tv_.get(), rw, rv, ow, ov, fl);
+        launch_ppi_rhs1(ctx.stream, P, ow, ov, rp, t_.get());
+        HL_.solve(ctx, t_.get(), oy, mg_, 0, fl);
+        launch_ppi_t(ctx.stream, P, ty, oy, ry, t2_.get());
+        // SPiHatOperator::apply_inverse (precond.cpp:254-260)
+        Hleft_.solve(ctx, t2_.get(), t3_.get(), mg_, 0, fl);
+        launch_op_apply(ctx.stream, P.L, t3_.get(), t_.get());
+        Hright_.solve(ctx, t_.get(), op, mg_, 0, fl);
+        launch_check("P_Pi apply");
+        return;
+    }
+    if (setup_kind_ == OC_PRECOND_PPI && !heat_) throw InvalidArgument("P_D/P_T not set up");
+    // BlockDiagPrecond (precond.cpp:202-212) / BlockTriPrecond (:214-230)
+    ChebWork w{cg_.get(), c0_.get(), c1_.get(), c2_.get()};
+    launch_chebyshev(ctx.stream, P, ry, ty, cheb_steps_, w, oy);
+    launch_control_2x2(ctx.stream, P, tw_.get(), tv_.get(), rw, rv, ow, ov, fl);
+    if (kind == OC_PRECOND_PT) {
+        launch_coupling(ctx.stream, P, oy, ow, ov, rp, t_.get());
+        schur_apply(t_.get(), op);
+    } else {
+        schur_apply(rp, op);
+    }
+    launch_check("block preconditioner apply");
+}
+
+void Problem::ensure_krylov(size_t count)
+{
+    const size_t n4 = 4 * (size_t)ny_;
+    bool grew = false;
+    while (V_.size() < count + 1) V_.emplace_back(n4);
+    while (Z_.size() < count) {
+        Z_.emplace_back(n4);
+        grew = true;
+    }
+    if (grew || Ztab_.size() < Z_.size()) {
+        std::vector<const double*> tab(Z_.size());
+        for (size_t i = 0; i < Z_.size(); ++i) tab[i] = Z_[i].get();
+        Ztab_.resize(std::max(Z_.size(), (size_t)1));
+        cuda_check(cudaMemcpyAsync(Ztab_.get(), tab.data(), tab.size() * sizeof(const double*),
+                                   cudaMemcpyHostToDevice, ctx.stream),
+                   "Ztab upload");
+        ctx.sync();
+    }
+}
+
+oc_solve_report Problem::gmres(const oc_ipm_params& p, int kind, const double* b, double* x)
+{
+    // krylov.cpp:133-212 (full GMRES; optional restart every p.gmres_restart)
+    oc_solve_report rep{};
+    const long long n = 4 * ny_;
+    const int maxit = p.linear_maxit;
+    const int restart = p.gmres_restart > 0 ? p.gmres_restart : maxit;
+    const int ld = std::max(restart, 1) + 1;
+    if (H_.size() < (size_t)ld * ld) H_.resize((size_t)ld * ld);
+    cs_.resize(ld); sn_.resize(ld); g_.resize(ld); yls_.resize(ld);
+    kw_.resize(n); kx2_.resize(n);
+    double* scal = scal_.get();
+    double* part = part_.get();
+    GmresDev G{H_.get(), cs_.get(), sn_.get(), g_.get(), yls_.get(), scal, stop_.get(), ld};
+
+    launch_fill(ctx.stream, x, 0.0, n);
+    launch_dot_partials(ctx.stream, b, b, n, part);
+    launch_finalize(ctx.stream, part, scal + 0, 1);
+    const double bnorm = read_scalar(scal + 0);
+    if (bnorm == 0.0) {
+        rep.converged = 1;
+        return rep;
+    }
+    double last_relres = 0.0;
+    int total = 0;
+    bool xbase = false;
+    while (total < maxit) {
+        // (re)start: r0 = b - A x (restart only), V0 = r0 / ||r0||, g0 = ||r0||
+        ensure_krylov(std::min(restart, maxit));
+        if (!xbase) {
+            launch_scale_inv(ctx.stream, b, scal + 0, V_[0].get(), n, nullptr);
+            launch_copy(ctx.stream, scal + 0, g_.get(), 1);
+        } else {
+            launch_copy(ctx.stream, x, kx2_.get(), n);
+            launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(), x,
+                       kw_.get(), nullptr, nullptr);
+            // r0 = b - A x (V1 as scratch), V0 = r0 / ||r0||, g0 = ||r0||
+            launch_copy(ctx.stream, b, V_[1].get(), n);
+            launch_fill(ctx.stream, scal + 6, 1.0, 1);
+            launch_axpy_neg(ctx.stream, scal + 6, kw_.get(), V_[1].get(), n);
+            launch_dot_partials(ctx.stream, V_[1].get(), V_[1].get(), n, part);
+            launch_finalize(ctx.stream, part, scal + 7, 1);
+            launch_scale_inv(ctx.stream, V_[1].get(), scal + 7, V_[0].get(), n, nullptr);
+            launch_copy(ctx.stream, scal + 7, g_.get(), 1);
+        }
+        cuda_check(cudaMemsetAsync(stop_.get(), 0, sizeof(int), ctx.stream), "memset");
+        for (int j = 0; j < restart && total < maxit; ++j) {
+            precond_apply(kind, V_[j].get(), Z_[j].get());
+            launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(),
+                       Z_[j].get(), kw_.get(), nullptr, nullptr);
+            for (int i = 0; i <= j; ++i) {
+                launch_dot_partials(ctx.stream, kw_.get(), V_[i].get(), n, part);
+                launch_mgs_step(ctx.stream, part, G, i, j, V_[i].get(), kw_.get(), n);
+            }
+            launch_dot_partials(ctx.stream, kw_.get(), kw_.get(), n, part);
+            launch_gmres_givens(ctx.stream, part, G, j);
+            launch_scale_inv(ctx.stream, kw_.get(), scal + 1, V_[j + 1].get(), n, stop_.get());
+            launch_combine(ctx.stream, Ztab_.get(), yls_.get(), j + 1, x, n,
+                           xbase ? kx2_.get() : nullptr);
+            launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(), x,
+                       nullptr, b, part);
+            launch_relres(ctx.stream, part, scal + 0, scal + 2);
+            launch_check("gmres iteration");
+            cuda_check(cudaMemcpyAsync(ctx.hscal, scal, 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                                       ctx.stream), "readback");
+            cuda_check(cudaMemcpyAsync(ctx.hflags, flags_.get(), sizeof(int),
+                                       cudaMemcpyDeviceToHost, ctx.stream), "readback");
+            cuda_check(cudaMemcpyAsync(ctx.hflags + 1, stop_.get(), sizeof(int),
+                                       cudaMemcpyDeviceToHost, ctx.stream), "readback");
+            ctx.sync();
+            check_flags(false);
+            const double hnext = ctx.hscal[1];
+            const double relres = ctx.hscal[2];
+            if (ctx.hflags[1]) {
+                // zero pivot: the reference breaks before rebuilding x (krylov.cpp:166-170)
+                std::snprintf(rep.message, sizeof(rep.message),
+                              "gmres: zero pivot in Hessenberg triangularization");
+                if (j > 0)
+                    launch_combine(ctx.stream, Ztab_.get(), yls_.get(), j, x, n,
+                                   xbase ? kx2_.get() : nullptr);
+                else if (xbase)
+                    launch_copy(ctx.stream, kx2_.get(), x, n);
+                else
+                    launch_fill(ctx.stream, x, 0.0, n);
+                rep.relative_residual = last_relres;
+                return rep;
+            }
+            ++total;
+            rep.iterations = total;
+            rep.relative_residual = relres;
+            last_relres = relres;
+            if (relres <= p.linear_tol) {
+                rep.converged = 1;
+                return rep;
+            }
+            if (hnext <= 1e-300) {
+                std::snprintf(rep.message, sizeof(rep.message),
+                              "gmres: Krylov space exhausted before tolerance");
+                return rep;
+            }
+        }
+        xbase = true; // restart from the current iterate
+    }
+    std::snprintf(rep.message, sizeof(rep.message), "gmres: max iterations reached");
+    return rep;
+}
+
+oc_solve_report Problem::minres(const oc_ipm_params& p, int kind, const double* b, double* x)
+{
+    // krylov.cpp:37-131
+    oc_solve_report rep{};
+    const long long n = 4 * ny_;
+    for (auto& v : kvec_) v.resize(n);
+    kw_.resize(n);
+    double* vprev = kvec_[0].get();
+    double* v = kvec_[1].get();
+    double* vnext = kvec_[2].get();
+    double* z = kvec_[3].get();
+    double* znext = kvec_[4].get();
+    double* wprev = kvec_[5].get();
+    double* w = kvec_[6].get();
+    double* wnext = kvec_[7].get();
+    double* az = kw_.get();
+    double* sc = scal_.get() + 16; // MINRES scalar slots
+    double* part = part_.get();
+    int* stop = stop_.get();
+
+    launch_fill(ctx.stream, x, 0.0, n);
+    launch_dot_partials(ctx.stream, b, b, n, part);
+    launch_finalize(ctx.stream, part, scal_.get() + 0, 1);
+    const double bnorm = read_scalar(scal_.get() + 0);
+    if (bnorm == 0.0) {
+        rep.converged = 1;
+        return rep;
+    }
+    launch_fill(ctx.stream, vprev, 0.0, n);
+    launch_copy(ctx.stream, b, v, n);
+    precond_apply(kind, v, z);
+    launch_dot_partials(ctx.stream, z, v, n, part);
+    launch_minres_setup(ctx.stream, part, sc);
+    cuda_check(cudaMemsetAsync(stop, 0, sizeof(int), ctx.stream), "memset");
+    const double gamma_sq = read_scalar(sc + 15);
+    check_flags(true);
+    if (!(gamma_sq > 0.0)) {
+        rep.breakdown = 1;
+        std::snprintf(rep.message, sizeof(rep.message),
+                      "minres: preconditioner not positive definite");
+        rep.relative_residual = 1.0;
+        return rep;
+    }
+    launch_fill(ctx.stream, wprev, 0.0, n);
+    launch_fill(ctx.stream, w, 0.0, n);
+    const double* tyk = has_sb_ ? ty_.get() : nullptr;
+    for (int j = 1; j <= p.linear_maxit; ++j) {
+        launch_scale_inv(ctx.stream, z, sc + 0, z, n, nullptr);
+        launch_kkt(ctx.stream, P, tyk, tw_.get(), tv_.get(), z, az, nullptr, nullptr);
+        launch_dot_partials(ctx.stream, az, z, n, part);
+        launch_minres_delta(ctx.stream, part, sc);
+        launch_minres_vnext(ctx.stream, az, v, vprev, vnext, sc, j == 1 ? 1 : 0, n);
+        precond_apply(kind, vnext, znext);
+        launch_dot_partials(ctx.stream, znext, vnext, n, part);
+        launch_minres_gamma(ctx.stream, part, sc, stop);
+        launch_minres_update(ctx.stream, z, wprev, w, wnext, x, sc, stop, n);
+        launch_minres_rotate(ctx.stream, sc, stop);
+        launch_kkt(ctx.stream, P, tyk, tw_.get(), tv_.get(), x, nullptr, b, part);
+        launch_relres(ctx.stream, part, scal_.get() + 0, scal_.get() + 2);
+        launch_check("minres iteration");
+        cuda_check(cudaMemcpyAsync(ctx.hscal, scal_.get(), 48 * sizeof(double),
+                                   cudaMemcpyDeviceToHost, ctx.stream), "readback");
+        cuda_check(cudaMemcpyAsync(ctx.hflags, flags_.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx.stream), "readback");
+        cuda_check(cudaMemcpyAsync(ctx.hflags + 1, stop, sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx.stream), "readback");
+        ctx.sync();
+        check_flags(false);
+        const double relres = ctx.hscal[2];
+        const int st = ctx.hflags[1];
+        if (st == 1) {
+            rep.breakdown = 1;
+            std::snprintf(rep.message, sizeof(rep.message),
+                          "minres: preconditioner lost definiteness");
+            rep.iterations = j;
+            rep.relative_residual = relres;
+            return rep;
+        }
+        if (st == 2) {
+            rep.iterations = j;
+            rep.relative_residual = relres;
+            rep.converged = relres <= p.linear_tol;
+            return rep;
+        }
+        std::swap(vprev, v);
+        std::swap(v, vnext);
+        std::swap(z, znext);
+        std::swap(wprev, w);
+        std::swap(w, wnext);
+        rep.iterations = j;
+        rep.relative_residual = relres;
+        if (relres <= p.linear_tol) {
+            rep.converged = 1;
+            return rep;
+        }
+        if (ctx.hscal[16 + 0] == 0.0) break; // gamma == 0: Krylov space exhausted
+    }
+    if (!rep.converged) std::snprintf(rep.message, sizeof(rep.message), "minres: max iterations reached");
+    return rep;
+}
+
+oc_solve_report Problem::newton_solve(const oc_ipm_params& p, const double* rhs, double* x)
+{
+    int kind;
+    bool use_gmres;
+    if (heat_) {
+        // make_spacetime_model supports gmres-pt (timedep.cpp:344-431); the
+        // block-diagonal MINRES variant is the BASELINE config-5 extension.
+        if (p.solver == OC_SOLVER_GMRES_PT) { kind = OC_PRECOND_PT; use_gmres = true; }
+        else if (p.solver == OC_SOLVER_MINRES_PD) { kind = OC_PRECOND_PD; use_gmres = false; }
+        else throw InvalidArgument("spacetime newton_solve: unsupported solver kind");
+    } else {
+        switch (p.solver) {
+        case OC_SOLVER_MINRES_PD:
+            if (partial_obs_) throw InvalidArgument("minres-pd requires a nonsingular (1,1) block");
+            kind = OC_PRECOND_PD; use_gmres = false; break;
+        case OC_SOLVER_GMRES_PT:
+            if (partial_obs_) throw InvalidArgument("gmres-pt requires a nonsingular (1,1) block");
+            kind = OC_PRECOND_PT; use_gmres = true; break;
+        case OC_SOLVER_GMRES_PPI:
+            kind = OC_PRECOND_PPI; use_gmres = true; break;
+        default:
+            throw InvalidArgument("newton_solve: the dense solver is a CPU verification path");
+        }
+    }
+    setup_precond(kind, p);
+    return use_gmres ? gmres(p, kind, rhs, x) : minres(p, kind, rhs, x);
+}
+
+void Problem::ipm_solve(const oc_ipm_params& p, oc_ipm_result* r)
+{
+    // ipm_solve (ipm.cpp:270-341)
+    if (!(p.alpha0 > 0.0 && p.alpha0 < 1.0))
+        throw InvalidArgument("ipm_solve: alpha0 must lie in (0,1)");
+    if (!(p.sigma > 0.0 && p.sigma < 1.0)) throw InvalidArgument("ipm_solve: sigma must lie in (0,1)");
+    if (p.mu0 <= 0.0) throw InvalidArgument("ipm_solve: mu0 must be positive");
+    cudaEvent_t es, ee, ns, ne;
+    cuda_check(cudaEventCreate(&es), "event");
+    cuda_check(cudaEventCreate(&ee), "event");
+    cuda_check(cudaEventCreate(&ns), "event");
+    cuda_check(cudaEventCreate(&ne), "event");
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() { for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]); }
+    };
+    cudaEvent_t evs[4] = {es, ee, ns, ne};
+    EvGuard guard{evs};
+
+    cuda_check(cudaMemsetAsync(flags_.get(), 0, sizeof(int), ctx.stream), "memset");
+    cudaEventRecord(es, ctx.stream);
+    launch_initial_point(ctx.stream, P, S);
+    double* norms = scal_.get() + 40;
+    double* steps = scal_.get() + 44;
+    launch_ipm_residuals(ctx.stream, P, S, p.mu0, part_.get(), norms);
+    cuda_check(cudaMemcpyAsync(ctx.hscal, norms, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx.stream), "readback");
+    ctx.sync();
+    double nrm[3] = {ctx.hscal[0], ctx.hscal[1], ctx.hscal[2]};
+    std::vector<oc_iter_record> recs;
+    recs.push_back({0, p.mu0, nrm[0], nrm[1], nrm[2], 0, 0.0, 1, 0.0});
+
+    double state_mu = p.mu0;
+    int k = 0;
+    auto converged = [&]() {
+        return nrm[0] <= p.eps_p && nrm[1] <= p.eps_d && nrm[2] <= p.eps_c && state_mu <= p.eps_c;
+    };
+    double mu = p.mu0;
+    long long total_lin = 0;
+    double newton_total = 0.0;
+    while (!converged() && k < p.max_iterations) {
+        mu = p.sigma * mu;
+        launch_theta(ctx.stream, P, S, flags_.get());
+        launch_newton_rhs(ctx.stream, P, S, mu, rhs_.get());
+        cudaEventRecord(ns, ctx.stream);
+        const oc_solve_report rep = newton_solve(p, rhs_.get(), sol_.get());
+        cudaEventRecord(ne, ctx.stream);
+        launch_recover_ratios(ctx.stream, P, S, mu, part_.get());
+        launch_step_lengths(ctx.stream, part_.get(), p.alpha0, steps);
+        launch_ipm_update(ctx.stream, P, S, steps, flags_.get());
+        state_mu = mu;
+        ++k;
+        launch_ipm_residuals(ctx.stream, P, S, mu, part_.get(), norms);
+        launch_check("ipm iteration");
+        cuda_check(cudaMemcpyAsync(ctx.hscal, norms, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx.stream), "readback");
+        cuda_check(cudaMemcpyAsync(ctx.hflags, flags_.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx.stream), "readback");
+        ctx.sync();
+        check_flags(false);
+        float nms = 0.f;
+        cudaEventElapsedTime(&nms, ns, ne);
+        newton_total += nms;
+        nrm[0] = ctx.hscal[0];
+        nrm[1] = ctx.hscal[1];
+        nrm[2] = ctx.hscal[2];
+        total_lin += rep.iterations;
+        recs.push_back({k, mu, nrm[0], nrm[1], nrm[2], rep.iterations, rep.relative_residual,
+                        rep.converged, (double)nms});
+    }
+    const bool conv = converged();
+    // outputs: objective, sparsity, vectors
+    double* obj = scal_.get() + 48;
+    launch_objective(ctx.stream, P, S, part_.get(), obj);
+    cudaEventRecord(ee, ctx.stream);
+    cuda_check(cudaMemcpyAsync(ctx.hscal, obj, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx.stream), "readback");
+    ctx.sync();
+    float sms = 0.f;
+    cudaEventElapsedTime(&sms, es, ee);
+    r->objective = ctx.hscal[0];
+    const double below = ctx.hscal[1];
+    r->l1 = ctx.hscal[2];
+    r->sparsity_pct = ny_ == 0 ? 100.0 : 100.0 * below / (double)ny_;
+    const long long all = (long long)(nx_ + 2) * (nx_ + 2);
+    r->nodal_sparsity_pct =
+        100.0 * (below + (double)((all - ns_) * nt_)) / (double)(all * nt_);
+    r->nli = k;
+    r->converged = conv ? 1 : 0;
+    r->av_li = k > 0 ? (double)total_lin / k : 0.0;
+    r->total_lin = total_lin;
+    r->mu = state_mu;
+    r->solve_ms = sms;
+    r->newton_ms = newton_total;
+    r->n_records = (int)recs.size();
+    if (r->records)
+        for (int i = 0; i < std::min(r->n_records, r->records_cap); ++i) r->records[i] = recs[i];
+    const size_t N = (size_t)ny_;
+    if (r->y) copy_any(ctx, r->y, y_.get(), N * sizeof(double));
+    if (r->z) copy_any(ctx, r->z, z_.get(), 2 * N * sizeof(double));
+    if (r->p) copy_any(ctx, r->p, p_.get(), N * sizeof(double));
+    if (r->lam_za) copy_any(ctx, r->lam_za, lza_.get(), 2 * N * sizeof(double));
+    if (r->lam_zb) copy_any(ctx, r->lam_zb, lzb_.get(), 2 * N * sizeof(double));
+    if (has_sb_) {
+        if (r->lam_ya) copy_any(ctx, r->lam_ya, lya_.get(), N * sizeof(double));
+        if (r->lam_yb) copy_any(ctx, r->lam_yb, lyb_.get(), N * sizeof(double));
+    }
+    if (r->u) {
+        launch_recover_control(ctx.stream, ny_, z_.get(), t_.get());
+        copy_any(ctx, r->u, t_.get(), N * sizeof(double));
+    }
+    ctx.sync();
+}
+
+void Problem::ipm_pieces(const double* y, const double* z, const double* pv, const double* lya,
+                         const double* lyb, const double* lza, const double* lzb, double mu_state,
+                         double mu_rhs, double* ty, double* tw, double* tv, double* r1, double* r2,
+                         double* r3, double* norms3)
+{
+    const size_t N = (size_t)ny_;
+    copy_any(ctx, y_.get(), y, N * 8);
+    copy_any(ctx, z_.get(), z, 2 * N * 8);
+    copy_any(ctx, p_.get(), pv, N * 8);
+    copy_any(ctx, lza_.get(), lza, 2 * N * 8);
+    copy_any(ctx, lzb_.get(), lzb, 2 * N * 8);
+    if (has_sb_) {
+        copy_any(ctx, lya_.get(), lya, N * 8);
+        copy_any(ctx, lyb_.get(), lyb, N * 8);
+    }
+    cuda_check(cudaMemsetAsync(flags_.get(), 0, sizeof(int), ctx.stream), "memset");
+    launch_theta(ctx.stream, P, S, flags_.get());
+    launch_newton_rhs(ctx.stream, P, S, mu_rhs, rhs_.get());
+    double* norms = scal_.get() + 40;
+    launch_ipm_residuals(ctx.stream, P, S, mu_state, part_.get(), norms);
+    if (ty) {
+        if (has_sb_) copy_any(ctx, ty, ty_.get(), N * 8);
+        else {
+            launch_fill(ctx.stream, t_.get(), 0.0, ny_);
+            copy_any(ctx, ty, t_.get(), N * 8);
+        }
+    }
+    if (tw) copy_any(ctx, tw, tw_.get(), N * 8);
+    if (tv) copy_any(ctx, tv, tv_.get(), N * 8);
+    if (r1) copy_any(ctx, r1, rhs_.get(), N * 8);
+    if (r2) copy_any(ctx, r2, rhs_.get() + N, 2 * N * 8);
+    if (r3) copy_any(ctx, r3, rhs_.get() + 3 * N, N * 8);
+    cuda_check(cudaMemcpyAsync(ctx.hscal, norms, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx.stream), "readback");
+    ctx.sync();
+    if (norms3) std::memcpy(norms3, ctx.hscal, 3 * sizeof(double));
+    check_flags(true);
+}
+
+double Problem::objective(const double* y, const double* z)
+{
+    const size_t N = (size_t)ny_;
+    copy_any(ctx, y_.get(), y, N * 8);
+    copy_any(ctx, z_.get(), z, 2 * N * 8);
+    double* obj = scal_.get() + 48;
+    launch_objective(ctx.stream, P, S, part_.get(), obj);
+    return read_scalar(obj);
+}
+
+void Problem::time_applies(int kind, int reps, double* kkt_ms, double* prec_ms)
+{
+    if (setup_kind_ < 0) throw InvalidArgument("preconditioner not set up");
+    const long long n = 4 * ny_;
+    kw_.resize(n);
+    kx2_.resize(n);
+    launch_fill(ctx.stream, kx2_.get(), 1.0, n);
+    // warm-up
+    kkt(kx2_.get(), kw_.get());
+    precond_apply(kind, kx2_.get(), kw_.get());
+    ctx.sync();
+    cudaEventRecord(ctx.ev0, ctx.stream);
+    for (int i = 0; i < reps; ++i) kkt(kx2_.get(), kw_.get());
+    cudaEventRecord(ctx.ev1, ctx.stream);
+    ctx.sync();
+    float a = 0.f;
+    cudaEventElapsedTime(&a, ctx.ev0, ctx.ev1);
+    cudaEventRecord(ctx.ev0, ctx.stream);
+    for (int i = 0; i < reps; ++i) precond_apply(kind, kx2_.get(), kw_.get());
+    cudaEventRecord(ctx.ev1, ctx.stream);
+    ctx.sync();
+    float b = 0.f;
+    cudaEventElapsedTime(&b, ctx.ev0, ctx.ev1);
+    *kkt_ms = a / reps;
+    *prec_ms = b / reps;
+    check_flags(true);
+}
+
+} // namespace ocb

@@ -1,0 +1,197 @@
+// Host orchestration of the device-resident IPM Newton solve.
+//
+// Everything here only enqueues kernels on the context stream; the host reads
+// back a handful of scalars once per Krylov iteration (convergence test) and
+// once per IPM iteration (residual norms, error flags).
+#pragma once
+
+#include "../../include/optcon_b200.h"
+#include "kernels.hpp"
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ocb {
+
+struct InvalidArgument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct RuntimeError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+template <typename T>
+class DevArray {
+public:
+    DevArray() = default;
+    explicit DevArray(size_t n) { resize(n); }
+    ~DevArray() { release(); }
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    DevArray(DevArray&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevArray& operator=(DevArray&& o) noexcept
+    {
+        if (this != &o) {
+            release();
+            p_ = o.p_; n_ = o.n_;
+            o.p_ = nullptr; o.n_ = 0;
+        }
+        return *this;
+    }
+    void resize(size_t n)
+    {
+        if (n == n_) return;
+        release();
+        if (n) cuda_check(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+        n_ = n;
+    }
+    void release()
+    {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    explicit operator bool() const { return p_ != nullptr; }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+using DVec = DevArray<double>;
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double* hscal = nullptr; // pinned host mirror (64 doubles)
+    int* hflags = nullptr;   // pinned host mirror (8 ints)
+    explicit Ctx(int dev);
+    ~Ctx();
+    void sync();
+};
+
+// Copy between host/device pointers of unknown kind (cudaMemcpyDefault).
+void copy_any(Ctx& c, void* dst, const void* src, size_t bytes);
+bool is_device_ptr(const void* p);
+
+struct MgParams {
+    int cycles = 3, pre = 5, post = 5;
+};
+
+// Geometric multigrid hierarchy (MgHierarchy, multigrid.hpp:43-64) for one
+// operator, or for `batch` operators of the same level (heat time blocks).
+class Hierarchy {
+public:
+    void allocate(int level, int batch = 1);
+    // Galerkin coarse operators R A P of the fine operator (per batch block the
+    // fine coef/diag pointers advance by fine_coef_stride / fine_diag_stride).
+    void build(Ctx& c, const Op9& fine, long long fine_coef_stride = 0,
+               long long fine_diag_stride = 0);
+    // Rediscretised coarse operators: base[k] (k = 1..K, 9 arrays each) plus
+    // the Galerkin-coarsened remainder fine - base(level) (multigrid.cpp:86-101).
+    void build_rediscretized(Ctx& c, const Op9& fine, const std::vector<const double*>& base);
+    // solve: `cycles` V-cycles from x = 0 with the divergence check.
+    void solve(Ctx& c, const double* b, double* x, const MgParams& p, int bt, int* flags);
+    // one smoothing sweep on the fine level (in place through the scratch buffer)
+    void smooth(Ctx& c, const double* b, double* x, bool forward, int bt);
+    int depth() const { return K_; }
+    int level() const { return level_; }
+    Op9 level_op(int k, int bt) const;
+    long long level_n(int k) const { return (long long)nx_[k] * nx_[k]; }
+
+private:
+    void vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_in, const MgParams& p,
+                int bt, int* flags);
+    BottomArgs bottom_args(int kfrom, int bt) const;
+
+    int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1;
+    std::vector<int> nx_;
+    Op9 fine_{};
+    long long fine_coef_stride_ = 0, fine_diag_stride_ = 0;
+    std::vector<DVec> coef_;        // [k] 9*n_k*batch, k >= 1
+    std::vector<DVec> rem_;         // rediscretised remainder chain, k >= 1 (batch 1)
+    DVec remfine_;                  // fine remainder fine - base(level), 9 arrays
+    std::vector<DVec> xa_, xb_, b_; // per level work (k >= 1); xb_[0] fine scratch
+    DVec lu_;
+    DevArray<int> perm_;
+    DVec part_, state_;
+    bool built_ = false;
+};
+
+class Problem {
+public:
+    Problem(Ctx& c, const oc_problem_desc& d);
+    oc_problem_info info() const;
+
+    // preconditioner setup from Theta already in ty_/tw_/tv_ (device)
+    void setup_precond(int kind, const oc_ipm_params& p);
+    void precond_apply(int kind, const double* r, double* out);
+    void schur_apply(const double* r, double* out);
+    void kkt(const double* x, double* out);
+    void set_theta(const double* ty, const double* tw, const double* tv);
+
+    oc_solve_report newton_solve(const oc_ipm_params& p, const double* rhs, double* x);
+    void ipm_solve(const oc_ipm_params& p, oc_ipm_result* r);
+    void ipm_pieces(const double* y, const double* z, const double* pv, const double* lya,
+                    const double* lyb, const double* lza, const double* lzb, double mu_state,
+                    double mu_rhs, double* ty, double* tw, double* tv, double* r1, double* r2,
+                    double* r3, double* norms3);
+    double objective(const double* y, const double* z);
+    void time_applies(int kind, int reps, double* kkt_ms, double* prec_ms);
+
+    Ctx& ctx;
+    ProbDev P{};
+    IpmDev S{};
+
+private:
+    void check_flags(bool sync_now = true);
+    void upload(DVec& dst, const double* src, size_t n);
+    oc_solve_report gmres(const oc_ipm_params& p, int kind, const double* b, double* x);
+    oc_solve_report minres(const oc_ipm_params& p, int kind, const double* b, double* x);
+    void time_schur(const double* r, double* out);
+    double read_scalar(const double* dptr);
+    void ensure_krylov(size_t count);
+
+    int level_ = 0, nx_ = 0, nt_ = 1;
+    long long ns_ = 0, ny_ = 0;
+    bool heat_ = false, has_sb_ = false, partial_obs_ = false, convdiff_ = false;
+    double eps_ = 0.0;
+    MgParams mg_{};
+    int cheb_steps_ = 20;
+
+    // operators and problem data
+    DVec Lc_, LTc_, Mobsc_, LTpMobs_;
+    std::vector<DVec> base_, baseT_;
+    DVec yd_, f_, za_, zb_, ya_, yb_, ld_, qw_;
+    // state and directions
+    DVec y_, z_, p_, lya_, lyb_, lza_, lzb_;
+    DVec dlya_, dlyb_, dlza_, dlzb_;
+    DVec ty_, tw_, tv_;
+    DVec rhs_, sol_;
+    // preconditioner
+    DVec mhat_, bracket_;
+    DVec cg_, c0_, c1_, c2_;
+    DVec t_, t2_, t3_, tf_, rblk_;
+    Hierarchy HF_, HFT_, HL_, Hleft_, Hright_, Hheat_;
+    bool HL_built_ = false;
+    int setup_kind_ = -1;
+    // Krylov
+    std::vector<DVec> V_, Z_;
+    DevArray<const double*> Ztab_;
+    DVec kw_, kx2_, kvec_[8];
+    DVec H_, cs_, sn_, g_, yls_;
+    // scalars
+    DVec part_, scal_;
+    DevArray<int> flags_, stop_;
+};
+
+} // namespace ocb
