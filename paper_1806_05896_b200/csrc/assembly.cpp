@@ -200,12 +200,12 @@ std::vector<double> transpose9(const std::vector<double>& coef, int level)
     for (int gy = 0; gy < nx; ++gy)
         for (int gx = 0; gx < nx; ++gx) {
             const long long i = (long long)gy * nx + gx;
-            for (int d = 0; d < 9; ++d) {
-                const int dx = d % 3 - 1, dy = d / 3 - 1;
-                const int jx = gx + dx, jy = gy + dy;
+            // T(i, i+off(e)) = A(j, i) with j = i+off(e), i.e. entry 8-e of row j
+            for (int e = 0; e < 9; ++e) {
+                const int jx = gx + e % 3 - 1, jy = gy + e / 3 - 1;
                 if (jx < 0 || jx >= nx || jy < 0 || jy >= nx) continue;
                 const long long j = (long long)jy * nx + jx;
-                t[(8 - d) * n + i] = coef[d * n + j];
+                t[e * n + i] = coef[(8 - e) * n + j];
             }
         }
     return t;

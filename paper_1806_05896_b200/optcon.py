@@ -358,9 +358,8 @@ class QpProblem:
             a.ptr(lam_ya, ny) if lam_ya is not None else None,
             a.ptr(lam_yb, ny) if lam_yb is not None else None, a.ptr(lam_za, 2 * ny),
             a.ptr(lam_zb, 2 * ny), C.c_double(mu_state), C.c_double(mu_rhs), *ptrs))
-        res = a.keep[-7:]
-        return dict(theta_y=res[0], theta_w=res[1], theta_v=res[2], r1=res[3], r2=res[4],
-                    r3=res[5], norms=res[6])
+        return dict(theta_y=outs[0], theta_w=outs[1], theta_v=outs[2], r1=outs[3], r2=outs[4],
+                    r3=outs[5], norms=outs[6])
 
     def objective(self, y, z) -> float:
         a = _Arg()
@@ -518,6 +517,7 @@ ASSEMBLE = {"mass": 0, "poisson": 1, "convdiff": 2, "partial_mass": 3, "lumped":
 def assemble9(what: str, level: int, eps: float = 0.1, obs=None) -> np.ndarray:
     """Host-side Q1 assembly (fem.cpp:142-180) into 9 coefficient arrays."""
     L = _lib.load()
+    Grid(level)  # Grid: level out of range (grid.hpp:20)
     n = ((1 << level) - 1) ** 2
     out = np.zeros(n if what == "lumped" else 9 * n)
     o = np.ascontiguousarray(obs if obs is not None else [0.0, 1.0, 0.0, 1.0], dtype=np.float64)
