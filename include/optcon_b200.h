@@ -114,6 +114,7 @@ typedef struct {
     long long kkt_dim;   /* 4 * ny */
     int has_state_bounds, partial_observation, symmetric_k;
     int level;
+    long long h2d_bytes;   /* bytes uploaded host->device by oc_problem_create */
 } oc_problem_info;
 
 const char* oc_last_error(void);
@@ -178,6 +179,17 @@ int oc_mg_smooth(oc_mg* mg, const double* b, double* x, int forward);
 /* ChebyshevSemiIteration(M(level), scale, extra, steps).apply(b) (chebyshev.cpp) */
 int oc_cheb_apply(oc_ctx* ctx, int level, double scale, const double* extra, int steps,
                   const double* b, double* x);
+/* Instrumentation (bench): kernel launches issued by this library so far;
+ * per-launch CUDA-event profiling on the solver stream of fine-level smoothing
+ * sweeps [0], KKT applies [1] and preconditioner applies [2]
+ * (oc_profile_read returns summed ms and counts, then resets); and stream
+ * events for timing a region on the solver stream (slots 0..7). */
+long long oc_launch_count(void);
+int oc_profile(oc_ctx* ctx, int enable);
+int oc_profile_read(oc_ctx* ctx, double* ms4, long long* counts4);
+int oc_event_record(oc_ctx* ctx, int slot);
+int oc_event_elapsed(oc_ctx* ctx, int slot_a, int slot_b, double* ms);
+
 /* Q1 assembly into 9 coefficient arrays (fem.cpp:142-180; what: 0 mass,
  * 1 poisson, 2 convdiff(eps), 3 partial mass(obs), 4 lumped diagonal (n)). Host only. */
 int oc_assemble9(int what, int level, double eps, const double* obs, double* coef);

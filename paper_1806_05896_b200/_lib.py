@@ -70,7 +70,7 @@ class ProblemInfoC(C.Structure):
     _fields_ = [
         ("n", C.c_int), ("nt", C.c_int), ("ny", C.c_longlong), ("kkt_dim", C.c_longlong),
         ("has_state_bounds", C.c_int), ("partial_observation", C.c_int),
-        ("symmetric_k", C.c_int), ("level", C.c_int),
+        ("symmetric_k", C.c_int), ("level", C.c_int), ("h2d_bytes", C.c_longlong),
     ]
 
 
@@ -93,7 +93,8 @@ EXPORTS = [
     "oc_ipm_solve", "oc_kkt_apply", "oc_precond_setup", "oc_precond_apply", "oc_schur_apply",
     "oc_newton_solve", "oc_ipm_pieces", "oc_objective", "oc_time_applies", "oc_mg_create",
     "oc_mg_solve", "oc_mg_depth", "oc_mg_level_matrix", "oc_mg_destroy", "oc_mg_smooth",
-    "oc_cheb_apply", "oc_assemble9",
+    "oc_cheb_apply", "oc_assemble9", "oc_launch_count", "oc_profile", "oc_profile_read",
+    "oc_event_record", "oc_event_elapsed",
 ]
 
 _lib = None
@@ -140,6 +141,12 @@ def load():
     L.oc_mg_smooth.argtypes = [vp, vp, vp, C.c_int]
     L.oc_cheb_apply.argtypes = [vp, C.c_int, C.c_double, vp, C.c_int, vp, vp]
     L.oc_assemble9.argtypes = [C.c_int, C.c_int, C.c_double, vp, vp]
+    L.oc_launch_count.restype = C.c_longlong
+    L.oc_launch_count.argtypes = []
+    L.oc_profile.argtypes = [vp, C.c_int]
+    L.oc_profile_read.argtypes = [vp, _dp, C.POINTER(C.c_longlong)]
+    L.oc_event_record.argtypes = [vp, C.c_int]
+    L.oc_event_elapsed.argtypes = [vp, C.c_int, C.c_int, _dp]
     _lib = L
     return L
 

@@ -388,6 +388,50 @@ int oc_cheb_apply(oc_ctx* c, int level, double scale, const double* extra, int s
     });
 }
 
+long long oc_launch_count(void) { return ocb::launch_count(); }
+
+int oc_profile(oc_ctx* c, int enable)
+{
+    return guarded([&] {
+        require(c, "oc_profile");
+        c->ctx.prof.on = enable != 0;
+    });
+}
+
+int oc_profile_read(oc_ctx* c, double* ms4, long long* counts4)
+{
+    return guarded([&] {
+        require(c, "oc_profile_read");
+        require(ms4, "oc_profile_read");
+        require(counts4, "oc_profile_read");
+        c->ctx.prof.read(ms4, counts4);
+    });
+}
+
+int oc_event_record(oc_ctx* c, int slot)
+{
+    return guarded([&] {
+        require(c, "oc_event_record");
+        if (slot < 0 || slot >= 8) throw ocb::InvalidArgument("oc_event_record: slot out of range");
+        ocb::cuda_check(cudaEventRecord(c->ctx.user_ev[slot], c->ctx.stream), "cudaEventRecord");
+    });
+}
+
+int oc_event_elapsed(oc_ctx* c, int a, int b, double* ms)
+{
+    return guarded([&] {
+        require(c, "oc_event_elapsed");
+        require(ms, "oc_event_elapsed");
+        if (a < 0 || a >= 8 || b < 0 || b >= 8)
+            throw ocb::InvalidArgument("oc_event_elapsed: slot out of range");
+        ocb::cuda_check(cudaEventSynchronize(c->ctx.user_ev[b]), "cudaEventSynchronize");
+        float t = 0.f;
+        ocb::cuda_check(cudaEventElapsedTime(&t, c->ctx.user_ev[a], c->ctx.user_ev[b]),
+                        "cudaEventElapsedTime");
+        *ms = t;
+    });
+}
+
 int oc_assemble9(int what, int level, double eps, const double* obs, double* coef)
 {
     return guarded([&] {

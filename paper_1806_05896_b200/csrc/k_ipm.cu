@@ -382,51 +382,62 @@ __global__ void k_recover_control(long long N, const double* __restrict__ z, dou
 
 void launch_theta(cudaStream_t s, const ProbDev& P, const IpmDev& S, int* flags)
 {
+    note_launch();
     k_theta<<<blocks_for(2 * P.ny), kT, 0, s>>>(P, S, flags);
 }
 
 void launch_newton_rhs(cudaStream_t s, const ProbDev& P, const IpmDev& S, double mu, double* rhs)
 {
+    note_launch();
     k_newton_rhs<<<blocks_for(P.ny), kT, 0, s>>>(P, S, mu, rhs);
 }
 
 void launch_recover_ratios(cudaStream_t s, const ProbDev& P, const IpmDev& S, double mu,
                            double* part)
 {
+    note_launch();
     k_recover_ratios<<<kRedBlocks, kRedThreads, 0, s>>>(P, S, mu, part);
 }
 
 void launch_step_lengths(cudaStream_t s, const double* part, double alpha0, double* steps)
 {
+    note_launch();
     k_step_lengths<<<1, 32, 0, s>>>(part, alpha0, steps);
 }
 
 void launch_ipm_update(cudaStream_t s, const ProbDev& P, const IpmDev& S, const double* steps,
                        int* flags)
 {
+    note_launch();
     k_ipm_update<<<blocks_for(2 * P.ny), kT, 0, s>>>(P, S, steps, flags);
 }
 
 void launch_ipm_residuals(cudaStream_t s, const ProbDev& P, const IpmDev& S, double mu,
                           double* part, double* norms)
 {
+    note_launch();
     k_ipm_residuals<<<kRedBlocks, kRedThreads, 0, s>>>(P, S, mu, part);
+    note_launch();
     k_residual_norms<<<1, 32, 0, s>>>(part, (double)P.ny, P.has_sb, norms);
 }
 
 void launch_objective(cudaStream_t s, const ProbDev& P, const IpmDev& S, double* part, double* out)
 {
+    note_launch();
     k_objective<<<kRedBlocks, kRedThreads, 0, s>>>(P, S, part);
+    note_launch();
     k_objective_final<<<1, 32, 0, s>>>(part, P.heat, P.alpha, out);
 }
 
 void launch_initial_point(cudaStream_t s, const ProbDev& P, const IpmDev& S)
 {
+    note_launch();
     k_initial_point<<<blocks_for(2 * P.ny), kT, 0, s>>>(P, S);
 }
 
 void launch_recover_control(cudaStream_t s, long long ny, const double* z, double* u)
 {
+    note_launch();
     k_recover_control<<<blocks_for(ny), kT, 0, s>>>(ny, z, u);
 }
 

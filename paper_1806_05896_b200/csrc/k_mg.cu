@@ -136,6 +136,7 @@ void sweep_launch(cudaStream_t s, const Op9& A, const double* b, const double* x
         attr = true;
     }
     dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
+    note_launch();
     k_gs_sweep<TX, TY, NS><<<grid, 256, smem, s>>>(A, b, x, xo, ec, forward ? 1 : 0,
                                                   zero_init ? 1 : 0);
 }
@@ -507,29 +508,35 @@ void launch_residual_restrict(cudaStream_t s, const Op9& A, const double* b, con
     constexpr int CX = 32, CY = 8;
     const int nxc = (A.nx - 1) / 2;
     dim3 grid((nxc + CX - 1) / CX, (nxc + CY - 1) / CY);
+    note_launch();
     k_residual_restrict<CX, CY><<<grid, CX * CY, 0, s>>>(A, b, x, bc, xc);
 }
 
 void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x)
 {
     const long long n = (long long)nx * nx;
+    note_launch();
     k_prolong_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nx, ec, x);
 }
 
 void launch_residual_norm_partials(cudaStream_t s, const Op9& A, const double* b,
                                    const double* x, double* part)
 {
+    note_launch();
     k_resid_norm_partials<<<kRedBlocks, kRedThreads, 0, s>>>(A, b, x, part);
 }
 
 void launch_mg_check(cudaStream_t s, const double* part, double* state, int* flags)
 {
+    note_launch();
     k_mg_check<<<1, 32, 0, s>>>(part, state, flags, 0);
 }
 
 void launch_norm_init(cudaStream_t s, const double* b, long long n, double* part, double* state)
 {
+    note_launch();
     k_sq_partials<<<kRedBlocks, kRedThreads, 0, s>>>(b, n, part);
+    note_launch();
     k_mg_check<<<1, 32, 0, s>>>(part, state, nullptr, 1);
 }
 
@@ -539,17 +546,20 @@ void launch_rap(cudaStream_t s, const Op9& fine, double* coarse, const double* b
     const int nxc = (fine.nx - 1) / 2;
     const long long nc = (long long)nxc * nxc;
     dim3 grid((unsigned)((nc + 127) / 128), batch);
+    note_launch();
     k_rap<<<grid, 128, 0, s>>>(fine, coarse, base, rem_out, fcs, fds, ccs);
 }
 
 void launch_remainder9(cudaStream_t s, const Op9& fine, const double* base9, double* rem9)
 {
     const long long n = (long long)fine.nx * fine.nx;
+    note_launch();
     k_remainder9<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(fine, base9, rem9);
 }
 
 void launch_coarse_lu(cudaStream_t s, const double* coef9, double* lu, int* perm, int batch)
 {
+    note_launch();
     k_coarse_lu<<<batch, 1, 0, s>>>(coef9, lu, perm, 81);
 }
 
@@ -571,6 +581,7 @@ void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double*
         attr = true;
     }
     if (smem > 200 * 1024) throw std::runtime_error("bottom solver: level too large for one CTA");
+    note_launch();
     k_bottom<<<1, kBottomThreads, smem, s>>>(a, b, x, cycles, pre, post, check ? 1 : 0, state,
                                              flags);
 }

@@ -332,6 +332,7 @@ __global__ void k_mhat(ProbDev P, const double* __restrict__ ty, const double* _
 void launch_mhat(cudaStream_t s, const ProbDev& P, const double* ty, const double* tw,
                  const double* tv, double* mhat, double* bracket, int* flags)
 {
+    note_launch();
     k_mhat<<<blocks_for(P.ny), kT, 0, s>>>(P, ty, tw, tv, mhat, bracket, flags);
 }
 
@@ -343,15 +344,15 @@ void launch_kkt(cudaStream_t s, const ProbDev& P, const double* ty, const double
     const long long N = P.ny;
     const unsigned grid = resid ? kRedBlocks : blocks_for(N);
     if (P.heat) {
-        if (has_ty && resid) k_kkt_heat<true, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else if (has_ty) k_kkt_heat<true, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else if (resid) k_kkt_heat<false, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else k_kkt_heat<false, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        if (has_ty && resid) { note_launch(); k_kkt_heat<true, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
+        else if (has_ty) { note_launch(); k_kkt_heat<true, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
+        else if (resid) { note_launch(); k_kkt_heat<false, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
+        else { note_launch(); k_kkt_heat<false, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
     } else {
-        if (has_ty && resid) k_kkt_steady<true, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else if (has_ty) k_kkt_steady<true, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else if (resid) k_kkt_steady<false, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else k_kkt_steady<false, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        if (has_ty && resid) { note_launch(); k_kkt_steady<true, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
+        else if (has_ty) { note_launch(); k_kkt_steady<true, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
+        else if (resid) { note_launch(); k_kkt_steady<false, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
+        else { note_launch(); k_kkt_steady<false, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
     }
 }
 
@@ -363,9 +364,11 @@ void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const d
     const double rho = (lmax - lmin) / (lmax + lmin);
     const unsigned grid = blocks_for(P.ny);
     if (steps <= 1) {
+        note_launch();
         k_cheb_init<<<grid, kT, 0, s>>>(P, b, e, omega, out);
         return;
     }
+    note_launch();
     k_cheb_init<<<grid, kT, 0, s>>>(P, b, e, omega, w.g);
     // rotating buffers R[s % 3]; the last step (s = steps) writes into out
     double* R[3] = {w.r0, w.r1, w.r2};
@@ -375,6 +378,7 @@ void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const d
         wk = (st == 2) ? 1.0 / (1.0 - 0.5 * rho * rho) : 1.0 / (1.0 - 0.25 * rho * rho * wk);
         const double* prev = (st == 2) ? nullptr : (st == 3 ? w.g : R[(st - 2) % 3]);
         const double* cur = (st == 2) ? w.g : R[(st - 1) % 3];
+        note_launch();
         k_cheb_step<<<grid, kT, 0, s>>>(P, e, omega, wk, prev, cur, w.g, R[st % 3]);
     }
 }
@@ -382,42 +386,48 @@ void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const d
 void launch_control_2x2(cudaStream_t s, const ProbDev& P, const double* tw, const double* tv,
                         const double* rw, const double* rv, double* vw, double* vv, int* flags)
 {
+    note_launch();
     k_control_2x2<<<blocks_for(P.ny), kT, 0, s>>>(P, tw, tv, rw, rv, vw, vv, flags);
 }
 
 void launch_coupling(cudaStream_t s, const ProbDev& P, const double* vy, const double* vw,
                      const double* vv, const double* rp, double* t)
 {
-    if (P.heat) k_coupling_heat<<<blocks_for(P.ny), kT, 0, s>>>(P, vy, vw, vv, rp, t);
-    else k_coupling_steady<<<blocks_for(P.ns), kT, 0, s>>>(P, vy, vw, vv, rp, t);
+    if (P.heat) { note_launch(); k_coupling_heat<<<blocks_for(P.ny), kT, 0, s>>>(P, vy, vw, vv, rp, t); }
+    else { note_launch(); k_coupling_steady<<<blocks_for(P.ns), kT, 0, s>>>(P, vy, vw, vv, rp, t); }
 }
 
 void launch_schur_middle(cudaStream_t s, const ProbDev& P, const double* ty, const double* t1,
                          double* t2)
 {
+    note_launch();
     k_schur_middle<<<blocks_for(P.ny), kT, 0, s>>>(P, ty, t1, t2);
 }
 
 void launch_ppi_rhs1(cudaStream_t s, const ProbDev& P, const double* vw, const double* vv,
                      const double* rp, double* rhs1)
 {
+    note_launch();
     k_ppi_rhs1<<<blocks_for(P.ns), kT, 0, s>>>(P, vw, vv, rp, rhs1);
 }
 
 void launch_ppi_t(cudaStream_t s, const ProbDev& P, const double* ty, const double* v1,
                   const double* ry, double* t)
 {
+    note_launch();
     k_ppi_t<<<blocks_for(P.ns), kT, 0, s>>>(P, ty, v1, ry, t);
 }
 
 void launch_op_apply(cudaStream_t s, const Op9& A, const double* x, double* y)
 {
+    note_launch();
     k_op_apply<<<blocks_for((long long)A.nx * A.nx), kT, 0, s>>>(A, x, y);
 }
 
 void launch_rhs_plus_mass(cudaStream_t s, const ProbDev& P, const double* r, const double* xnb,
                           double* rhs)
 {
+    note_launch();
     k_rhs_plus_mass<<<blocks_for(P.ns), kT, 0, s>>>(P, r, xnb, rhs);
 }
 

@@ -234,80 +234,93 @@ __global__ void k_minres_rotate(double* sc, const int* stop)
 void launch_dot_partials(cudaStream_t s, const double* x, const double* y, long long n,
                          double* part)
 {
+    note_launch();
     k_dot_partials<<<kRedBlocks, kRedThreads, 0, s>>>(x, y, n, part);
 }
 
 void launch_finalize(cudaStream_t s, const double* part, double* dst, int mode)
 {
+    note_launch();
     k_finalize<<<1, 32, 0, s>>>(part, dst, mode);
 }
 
 void launch_copy(cudaStream_t s, const double* x, double* y, long long n)
 {
-    if (n > 0) k_copy<<<blocks_for(n), kT, 0, s>>>(x, y, n);
+    if (n > 0) { note_launch(); k_copy<<<blocks_for(n), kT, 0, s>>>(x, y, n); }
 }
 
 void launch_fill(cudaStream_t s, double* x, double v, long long n)
 {
-    if (n > 0) k_fill<<<blocks_for(n), kT, 0, s>>>(x, v, n);
+    if (n > 0) { note_launch(); k_fill<<<blocks_for(n), kT, 0, s>>>(x, v, n); }
 }
 
 void launch_scale_inv(cudaStream_t s, const double* x, const double* den, double* y, long long n,
                       const int* stop)
 {
+    note_launch();
     k_scale_inv<<<blocks_for(n), kT, 0, s>>>(x, den, y, n, stop);
 }
 
 void launch_axpy_neg(cudaStream_t s, const double* h, const double* v, double* w, long long n)
 {
+    note_launch();
     k_axpy_neg<<<blocks_for(n), kT, 0, s>>>(h, v, w, n);
 }
 
 void launch_combine(cudaStream_t s, const double* const* Ztab, const double* y, int m, double* x,
                     long long n, const double* xbase)
 {
+    note_launch();
     k_combine<<<blocks_for(n), kT, 0, s>>>(Ztab, y, m, x, n, xbase);
 }
 
 void launch_add(cudaStream_t s, const double* a, const double* b, double* out, long long n)
 {
+    note_launch();
     k_add<<<blocks_for(n), kT, 0, s>>>(a, b, out, n);
 }
 
 void launch_mgs_step(cudaStream_t s, const double* part, const GmresDev& G, int i, int j,
                      const double* vi, double* w, long long n)
 {
+    note_launch();
     k_mgs_step<<<kRedBlocks * 4, kT, 0, s>>>(part, G.H, G.ld, i, j, vi, w, n);
 }
 
 void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j)
 {
+    note_launch();
     k_gmres_givens<<<1, 32, 0, s>>>(part, G, j);
 }
 
 void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst)
 {
+    note_launch();
     k_relres<<<1, 32, 0, s>>>(part, bnorm, dst);
 }
 
 void launch_minres_setup(cudaStream_t s, const double* part, double* sc)
 {
+    note_launch();
     k_minres_setup<<<1, 32, 0, s>>>(part, sc);
 }
 
 void launch_minres_delta(cudaStream_t s, const double* part, double* sc)
 {
+    note_launch();
     k_minres_delta<<<1, 32, 0, s>>>(part, sc);
 }
 
 void launch_minres_vnext(cudaStream_t s, const double* az, const double* v, const double* vprev,
                          double* vnext, const double* sc, int first, long long n)
 {
+    note_launch();
     k_minres_vnext<<<blocks_for(n), kT, 0, s>>>(az, v, vprev, vnext, sc, first, n);
 }
 
 void launch_minres_gamma(cudaStream_t s, const double* part, double* sc, int* stop)
 {
+    note_launch();
     k_minres_gamma<<<1, 32, 0, s>>>(part, sc, stop);
 }
 
@@ -315,11 +328,13 @@ void launch_minres_update(cudaStream_t s, const double* z, const double* wprev, 
                           double* wnext, double* x, const double* sc, const int* stop,
                           long long n)
 {
+    note_launch();
     k_minres_update<<<blocks_for(n), kT, 0, s>>>(z, wprev, w, wnext, x, sc, stop, n);
 }
 
 void launch_minres_rotate(cudaStream_t s, double* sc, const int* stop)
 {
+    note_launch();
     k_minres_rotate<<<1, 1, 0, s>>>(sc, stop);
 }
 

@@ -6,6 +6,10 @@
 
 namespace ocb {
 
+// Count of kernel launches issued by this library (bench "gpu_launches").
+void note_launch();
+long long launch_count();
+
 // ---------------------------------------------------------------- multigrid
 struct MgLevelDev {
     Op9 op;          // level operator (fine: constant stencil + diag, coarse: 9 arrays)

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <atomic>
 #include <cstring>
 
 namespace ocb {
@@ -24,6 +25,49 @@ void cuda_check(cudaError_t e, const char* what)
 
 static void launch_check(const char* what) { cuda_check(cudaGetLastError(), what); }
 
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+int Profiler::begin(cudaStream_t s, int cat)
+{
+    if (used == spans.size()) {
+        Span sp;
+        cuda_check(cudaEventCreate(&sp.a), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&sp.b), "cudaEventCreate");
+        spans.push_back(sp);
+    }
+    spans[used].cat = cat;
+    cudaEventRecord(spans[used].a, s);
+    return (int)used++;
+}
+
+void Profiler::end(cudaStream_t s, int idx) { cudaEventRecord(spans[idx].b, s); }
+
+void Profiler::read(double* ms, long long* counts)
+{
+    for (int k = 0; k < kProfCats; ++k) {
+        ms[k] = 0.0;
+        counts[k] = 0;
+    }
+    for (size_t i = 0; i < used; ++i) {
+        cuda_check(cudaEventSynchronize(spans[i].b), "cudaEventSynchronize");
+        float t = 0.f;
+        cuda_check(cudaEventElapsedTime(&t, spans[i].a, spans[i].b), "cudaEventElapsedTime");
+        ms[spans[i].cat] += t;
+        counts[spans[i].cat] += 1;
+    }
+    used = 0;
+}
+
+Profiler::~Profiler()
+{
+    for (auto& s : spans) {
+        cudaEventDestroy(s.a);
+        cudaEventDestroy(s.b);
+    }
+}
+
 Ctx::Ctx(int dev) : device(dev)
 {
     int count = 0;
@@ -33,6 +77,7 @@ Ctx::Ctx(int dev) : device(dev)
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaEventCreate(&ev0), "cudaEventCreate");
     cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
+    for (auto& e : user_ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     cuda_check(cudaMallocHost(&hscal, 64 * sizeof(double)), "cudaMallocHost");
     cuda_check(cudaMallocHost(&hflags, 8 * sizeof(int)), "cudaMallocHost");
 }
@@ -44,6 +89,8 @@ Ctx::~Ctx()
     if (hflags) cudaFreeHost(hflags);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    for (auto& e : user_ev)
+        if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -194,7 +241,10 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
     for (int i = 0; i < p.pre; ++i) {
         ++s;
         double* out = outbuf(s);
-        launch_gs_sweep(c.stream, A, b, cur, out, true, cur == nullptr, nullptr);
+        {
+            ProfScope ps(c, k == 0 ? kProfSweep : kProfCats);
+            launch_gs_sweep(c.stream, A, b, cur, out, true, cur == nullptr, nullptr);
+        }
         cur = out;
     }
     if (!cur) {
@@ -212,7 +262,12 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
     for (int i = 0; i < p.post; ++i) {
         ++s;
         double* out = outbuf(s);
-        launch_gs_sweep(c.stream, A, b, cur, out, false, false, i == 0 ? ec : nullptr);
+        {
+            // the first post sweep also applies the prolongation (fused); count
+            // it as a sweep only when it is a plain one
+            ProfScope ps(c, (k == 0 && i > 0) ? kProfSweep : kProfCats);
+            launch_gs_sweep(c.stream, A, b, cur, out, false, false, i == 0 ? ec : nullptr);
+        }
         cur = out;
     }
 }
@@ -278,6 +333,7 @@ void Problem::upload(DVec& dst, const double* src, size_t n)
 {
     dst.resize(n);
     copy_any(ctx, dst.get(), src, n * sizeof(double));
+    h2d_bytes_ += (long long)(n * sizeof(double));
 }
 
 Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
@@ -504,6 +560,7 @@ oc_problem_info Problem::info() const
     i.partial_observation = partial_obs_;
     i.symmetric_k = convdiff_ ? 0 : 1;
     i.level = level_;
+    i.h2d_bytes = h2d_bytes_;
     return i;
 }
 
@@ -785,9 +842,15 @@ oc_solve_report Problem::gmres(const oc_ipm_params& p, int kind, const double* b
         }
         cuda_check(cudaMemsetAsync(stop_.get(), 0, sizeof(int), ctx.stream), "memset");
         for (int j = 0; j < restart && total < maxit; ++j) {
-            precond_apply(kind, V_[j].get(), Z_[j].get());
-            launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(),
-                       Z_[j].get(), kw_.get(), nullptr, nullptr);
+            {
+                ProfScope ps(ctx, kProfPrec);
+                precond_apply(kind, V_[j].get(), Z_[j].get());
+            }
+            {
+                ProfScope ps(ctx, kProfKkt);
+                launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(),
+                           Z_[j].get(), kw_.get(), nullptr, nullptr);
+            }
             for (int i = 0; i <= j; ++i) {
                 launch_dot_partials(ctx.stream, kw_.get(), V_[i].get(), n, part);
                 launch_mgs_step(ctx.stream, part, G, i, j, V_[i].get(), kw_.get(), n);
@@ -893,11 +956,17 @@ oc_solve_report Problem::minres(const oc_ipm_params& p, int kind, const double* 
     const double* tyk = has_sb_ ? ty_.get() : nullptr;
     for (int j = 1; j <= p.linear_maxit; ++j) {
         launch_scale_inv(ctx.stream, z, sc + 0, z, n, nullptr);
-        launch_kkt(ctx.stream, P, tyk, tw_.get(), tv_.get(), z, az, nullptr, nullptr);
+        {
+            ProfScope ps(ctx, kProfKkt);
+            launch_kkt(ctx.stream, P, tyk, tw_.get(), tv_.get(), z, az, nullptr, nullptr);
+        }
         launch_dot_partials(ctx.stream, az, z, n, part);
         launch_minres_delta(ctx.stream, part, sc);
         launch_minres_vnext(ctx.stream, az, v, vprev, vnext, sc, j == 1 ? 1 : 0, n);
-        precond_apply(kind, vnext, znext);
+        {
+            ProfScope ps(ctx, kProfPrec);
+            precond_apply(kind, vnext, znext);
+        }
         launch_dot_partials(ctx.stream, znext, vnext, n, part);
         launch_minres_gamma(ctx.stream, part, sc, stop);
         launch_minres_update(ctx.stream, z, wprev, w, wnext, x, sc, stop, n);

@@ -68,15 +68,49 @@ private:
 };
 using DVec = DevArray<double>;
 
+// Per-launch CUDA-event spans on the solver stream for the bench's in-situ
+// kernel timing (fine-level smoothing sweeps, KKT applies, P applies).
+enum ProfCat { kProfSweep = 0, kProfKkt = 1, kProfPrec = 2, kProfNewton = 3, kProfCats = 4 };
+struct Profiler {
+    bool on = false;
+    struct Span {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int cat = 0;
+    };
+    std::vector<Span> spans;
+    size_t used = 0;
+    int begin(cudaStream_t s, int cat);
+    void end(cudaStream_t s, int idx);
+    // sum elapsed per category (syncs), then reset
+    void read(double* ms, long long* counts);
+    ~Profiler();
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t user_ev[8] = {};
     double* hscal = nullptr; // pinned host mirror (64 doubles)
     int* hflags = nullptr;   // pinned host mirror (8 ints)
+    Profiler prof;
     explicit Ctx(int dev);
     ~Ctx();
     void sync();
+};
+
+// RAII span: no-op unless profiling is on
+struct ProfScope {
+    Ctx& c;
+    int idx;
+    ProfScope(Ctx& cx, int cat)
+        : c(cx), idx((cx.prof.on && cat < kProfCats) ? cx.prof.begin(cx.stream, cat) : -1)
+    {
+    }
+    ~ProfScope()
+    {
+        if (idx >= 0) c.prof.end(c.stream, idx);
+    }
 };
 
 // Copy between host/device pointers of unknown kind (cudaMemcpyDefault).
@@ -163,6 +197,7 @@ private:
 
     int level_ = 0, nx_ = 0, nt_ = 1;
     long long ns_ = 0, ny_ = 0;
+    long long h2d_bytes_ = 0;
     bool heat_ = false, has_sb_ = false, partial_obs_ = false, convdiff_ = false;
     double eps_ = 0.0;
     MgParams mg_{};

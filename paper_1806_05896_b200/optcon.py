@@ -72,6 +72,30 @@ class Context:
     def synchronize(self):
         _lib.check(self._L.oc_synchronize(self.h))
 
+    # instrumentation (bench)
+    def record(self, slot: int):
+        """Record CUDA event `slot` (0..7) on the solver stream."""
+        _lib.check(self._L.oc_event_record(self.h, slot))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_double()
+        _lib.check(self._L.oc_event_elapsed(self.h, a, b, C.byref(ms)))
+        return ms.value
+
+    def profile(self, enable: bool):
+        _lib.check(self._L.oc_profile(self.h, int(enable)))
+
+    def profile_read(self):
+        """{'sweep'|'kkt'|'prec': (total_ms, count)} since the last read."""
+        ms = (C.c_double * 4)()
+        cnt = (C.c_longlong * 4)()
+        _lib.check(self._L.oc_profile_read(self.h, ms, cnt))
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(("sweep", "kkt", "prec", "newton"))}
+
+    @staticmethod
+    def launch_count() -> int:
+        return int(_lib.load().oc_launch_count())
+
     def close(self):
         if getattr(self, "h", None):
             self._L.oc_destroy(self.h)
@@ -282,6 +306,7 @@ class QpProblem:
         self.has_state_bounds = bool(info.has_state_bounds)
         self.partial_observation = bool(info.partial_observation)
         self.level = info.level
+        self.h2d_bytes = int(info.h2d_bytes)
         self.grid = grid
         self.problem = problem
 
