@@ -189,6 +189,13 @@ int oc_profile(oc_ctx* ctx, int enable);
 int oc_profile_read(oc_ctx* ctx, double* ms4, long long* counts4);
 int oc_event_record(oc_ctx* ctx, int slot);
 int oc_event_elapsed(oc_ctx* ctx, int slot_a, int slot_b, double* ms);
+/* elapsed ms from event slot_a of ctx_a to event slot_b of ctx_b (same device;
+ * used to time concurrent solves on several contexts' streams) */
+int oc_event_elapsed_between(oc_ctx* ctx_a, int slot_a, oc_ctx* ctx_b, int slot_b, double* ms);
+/* Tuning aid: enable/disable %globaltimer phase stamps inside the cluster
+ * multigrid bottom kernel and read the last launch's 64 stamps (CTA 0: 0..31,
+ * CTA 1: 32..63; 0 = not reached). out64 may be NULL. */
+int oc_debug_cluster_probes(int enable, unsigned long long* out64);
 
 /* Q1 assembly into 9 coefficient arrays (fem.cpp:142-180; what: 0 mass,
  * 1 poisson, 2 convdiff(eps), 3 partial mass(obs), 4 lumped diagonal (n)). Host only. */

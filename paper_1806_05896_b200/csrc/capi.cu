@@ -348,7 +348,11 @@ int oc_mg_smooth(oc_mg* m, const double* b, double* x, int forward)
     });
 }
 
-void oc_mg_destroy(oc_mg* m) { delete m; }
+void oc_mg_destroy(oc_mg* m)
+{
+    if (m && m->ctx) cudaStreamSynchronize(m->ctx->stream);
+    delete m;
+}
 
 int oc_cheb_apply(oc_ctx* c, int level, double scale, const double* extra, int steps,
                   const double* b, double* x)
@@ -390,6 +394,11 @@ int oc_cheb_apply(oc_ctx* c, int level, double scale, const double* extra, int s
 
 long long oc_launch_count(void) { return ocb::launch_count(); }
 
+int oc_debug_cluster_probes(int enable, unsigned long long* out64)
+{
+    return guarded([&] { ocb::cluster_probes(enable, out64); });
+}
+
 int oc_profile(oc_ctx* c, int enable)
 {
     return guarded([&] {
@@ -427,6 +436,23 @@ int oc_event_elapsed(oc_ctx* c, int a, int b, double* ms)
         ocb::cuda_check(cudaEventSynchronize(c->ctx.user_ev[b]), "cudaEventSynchronize");
         float t = 0.f;
         ocb::cuda_check(cudaEventElapsedTime(&t, c->ctx.user_ev[a], c->ctx.user_ev[b]),
+                        "cudaEventElapsedTime");
+        *ms = t;
+    });
+}
+
+int oc_event_elapsed_between(oc_ctx* ca, int a, oc_ctx* cb, int b, double* ms)
+{
+    return guarded([&] {
+        require(ca, "oc_event_elapsed_between");
+        require(cb, "oc_event_elapsed_between");
+        require(ms, "oc_event_elapsed_between");
+        if (a < 0 || a >= 8 || b < 0 || b >= 8)
+            throw ocb::InvalidArgument("oc_event_elapsed_between: slot out of range");
+        ocb::cuda_check(cudaEventSynchronize(ca->ctx.user_ev[a]), "cudaEventSynchronize");
+        ocb::cuda_check(cudaEventSynchronize(cb->ctx.user_ev[b]), "cudaEventSynchronize");
+        float t = 0.f;
+        ocb::cuda_check(cudaEventElapsedTime(&t, ca->ctx.user_ev[a], cb->ctx.user_ev[b]),
                         "cudaEventElapsedTime");
         *ms = t;
     });

@@ -63,6 +63,17 @@ void launch_coarse_lu(cudaStream_t s, const double* coef9, double* lu, int* perm
 void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double* x, int cycles,
                    int pre, int post, bool check, double* state, int* flags);
 
+// Cluster-resident bottom (k_mg_cluster.cu): levels <= 7 in one 16-CTA
+// thread-block cluster with distributed shared memory. ops[0] is the top
+// level handled (level 7 or 6).
+using ClusterArgs = BottomArgs;
+constexpr int kClusterTopLevel = 7;
+bool cluster_bottom_supported();
+// tuning aid: enable %globaltimer phase probes; read the last launch's stamps
+void cluster_probes(int enable, unsigned long long* out64);
+void launch_bottom_cluster(cudaStream_t s, const ClusterArgs& a, const double* b, double* x,
+                           int cycles, int pre, int post, bool check, double* state, int* flags);
+
 } // namespace ocb
 
 namespace ocb {

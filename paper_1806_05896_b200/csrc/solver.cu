@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <mutex>
 #include <cstring>
 
 namespace ocb {
@@ -24,6 +25,31 @@ void cuda_check(cudaError_t e, const char* what)
 }
 
 static void launch_check(const char* what) { cuda_check(cudaGetLastError(), what); }
+
+void* pool_alloc(size_t bytes)
+{
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long keep = ~0ull; // keep freed blocks pooled
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+    void* p = nullptr;
+    cuda_check(cudaMallocAsync(&p, bytes, cudaStreamPerThread), "cudaMallocAsync");
+    // the allocation is ordered on the per-thread stream; make it usable from
+    // the solver stream without a device-wide synchronisation
+    cuda_check(cudaStreamSynchronize(cudaStreamPerThread), "cudaStreamSynchronize");
+    return p;
+}
+
+void pool_free(void* p)
+{
+    cudaFreeAsync(p, cudaStreamPerThread);
+}
 
 static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -123,8 +149,12 @@ void Hierarchy::allocate(int level, int batch)
     K_ = level - 2;
     nx_.assign(K_ + 1, 0);
     for (int k = 0; k <= K_; ++k) nx_[k] = (1 << (level - k)) - 1;
+    // levels <= 7 run in the 16-CTA cluster kernel when the top of that range
+    // is a slab level (>= 6); otherwise levels <= 6 in the single-CTA kernel
+    cluster_ = level >= 6 && cluster_bottom_supported();
+    const int top = cluster_ ? kClusterTopLevel : kBottomTopLevel;
     kb_ = 0;
-    while (level - kb_ > kBottomTopLevel) ++kb_;
+    while (level - kb_ > top) ++kb_;
     coef_.clear();
     coef_.resize(K_ + 1);
     xa_.clear();
@@ -222,8 +252,12 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
                        const MgParams& p, int bt, int* flags)
 {
     if (k == kb_) {
-        launch_bottom(c.stream, bottom_args(kb_, bt), b, xout, 1, p.pre, p.post, false, nullptr,
-                      flags);
+        if (cluster_)
+            launch_bottom_cluster(c.stream, bottom_args(kb_, bt), b, xout, 1, p.pre, p.post, false,
+                                  nullptr, flags);
+        else
+            launch_bottom(c.stream, bottom_args(kb_, bt), b, xout, 1, p.pre, p.post, false,
+                          nullptr, flags);
         return;
     }
     const Op9 A = level_op(k, bt);
@@ -276,8 +310,12 @@ void Hierarchy::solve(Ctx& c, const double* b, double* x, const MgParams& p, int
 {
     const long long n = level_n(0);
     if (kb_ == 0) {
-        launch_bottom(c.stream, bottom_args(0, bt), b, x, p.cycles, p.pre, p.post, true,
-                      state_.get(), flags);
+        if (cluster_)
+            launch_bottom_cluster(c.stream, bottom_args(0, bt), b, x, p.cycles, p.pre, p.post,
+                                  true, state_.get(), flags);
+        else
+            launch_bottom(c.stream, bottom_args(0, bt), b, x, p.cycles, p.pre, p.post, true,
+                          state_.get(), flags);
         launch_check("multigrid bottom solve");
         return;
     }

@@ -27,6 +27,13 @@ struct CudaFailure : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Device memory comes from the stream-ordered pool allocator on the per-thread
+// stream: cudaFree would synchronise the whole device and serialise concurrent
+// solves (one context per host thread); pooled blocks are also reused across
+// problems. Owners synchronise their solver stream before releasing memory.
+void* pool_alloc(size_t bytes);
+void pool_free(void* p);
+
 template <typename T>
 class DevArray {
 public:
@@ -49,12 +56,12 @@ public:
     {
         if (n == n_) return;
         release();
-        if (n) cuda_check(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+        if (n) p_ = static_cast<T*>(pool_alloc(n * sizeof(T)));
         n_ = n;
     }
     void release()
     {
-        if (p_) cudaFree(p_);
+        if (p_) pool_free(p_);
         p_ = nullptr;
         n_ = 0;
     }
@@ -148,6 +155,7 @@ private:
     BottomArgs bottom_args(int kfrom, int bt) const;
 
     int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1;
+    bool cluster_ = false;  // bottom levels run in the 16-CTA cluster kernel
     std::vector<int> nx_;
     Op9 fine_{};
     long long fine_coef_stride_ = 0, fine_diag_stride_ = 0;
@@ -164,6 +172,7 @@ private:
 class Problem {
 public:
     Problem(Ctx& c, const oc_problem_desc& d);
+    ~Problem() { cudaStreamSynchronize(ctx.stream); } // before members return memory to the pool
     oc_problem_info info() const;
 
     // preconditioner setup from Theta already in ty_/tw_/tv_ (device)

@@ -82,6 +82,12 @@ class Context:
         _lib.check(self._L.oc_event_elapsed(self.h, a, b, C.byref(ms)))
         return ms.value
 
+    def elapsed_ms_to(self, a: int, other: "Context", b: int) -> float:
+        """ms from this context's event `a` to `other`'s event `b` (same device)."""
+        ms = C.c_double()
+        _lib.check(self._L.oc_event_elapsed_between(self.h, a, other.h, b, C.byref(ms)))
+        return ms.value
+
     def profile(self, enable: bool):
         _lib.check(self._L.oc_profile(self.h, int(enable)))
 
