@@ -394,6 +394,17 @@ int oc_cheb_apply(oc_ctx* c, int level, double scale, const double* extra, int s
 
 long long oc_launch_count(void) { return ocb::launch_count(); }
 
+int oc_set_tuning(const char* name, int value)
+{
+    return guarded([&] {
+        require(name, "oc_set_tuning");
+        const std::string k = name;
+        if (k == "sweep_tile") ocb::g_sweep_tile = value;
+        else if (k == "sweep_fuse") ocb::g_sweep_fuse = value;
+        else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
+    });
+}
+
 int oc_debug_cluster_probes(int enable, unsigned long long* out64)
 {
     return guarded([&] { ocb::cluster_probes(enable, out64); });

@@ -1,0 +1,355 @@
+// Multi-CTA multigrid kernels for the large levels (>= 8) (sm_100a, FP64).
+//
+// k_sweep<TX,TY,NS,VAR>: NS symmetric-colour Gauss-Seidel sweeps (4 colour
+// passes each, multigrid.cpp:44-66 restated as the 4-colour variant) over one
+// TX x TY output tile per CTA. The tile plus a halo of 4*NS nodes is staged in
+// shared memory with asynchronous copies (cp.async, all in flight at once):
+// x, b, the reciprocal diagonal and, for variable operators, the 8
+// off-diagonal coefficient planes. Pass q then updates the colour nodes of the
+// tile grown by 4*NS-1-q entirely from shared memory, so after all passes the
+// tile is exact without inter-CTA synchronisation (redundant halo work).
+// Threads form a 32x8 grid mapped onto the colour sub-lattice (no division).
+//
+// k_resid_restrict<VAR>: r = b - A x on the fine nodes of a coarse tile (x and
+// coefficients staged the same way), then rc = R r with R = P^T
+// (multigrid.cpp:120-123); also zeroes the coarse iterate.
+#include "kernels.hpp"
+
+namespace ocb {
+
+namespace {
+
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst_smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+__device__ __forceinline__ double prolong_at2(const double* __restrict__ ec, int nxc, int gx, int gy)
+{
+    int px[2], py[2];
+    double wx[2], wy[2];
+    int cxn = 0, cyn = 0;
+    if (gx & 1) { px[0] = (gx - 1) >> 1; wx[0] = 1.0; cxn = 1; }
+    else {
+        if (gx / 2 - 1 >= 0) { px[cxn] = gx / 2 - 1; wx[cxn++] = 0.5; }
+        if (gx / 2 < nxc) { px[cxn] = gx / 2; wx[cxn++] = 0.5; }
+    }
+    if (gy & 1) { py[0] = (gy - 1) >> 1; wy[0] = 1.0; cyn = 1; }
+    else {
+        if (gy / 2 - 1 >= 0) { py[cyn] = gy / 2 - 1; wy[cyn++] = 0.5; }
+        if (gy / 2 < nxc) { py[cyn] = gy / 2; wy[cyn++] = 0.5; }
+    }
+    double e = 0.0;
+    for (int a = 0; a < cyn; ++a)
+        for (int c = 0; c < cxn; ++c) e += (wx[c] * wy[a]) * ec[(long long)py[a] * nxc + px[c]];
+    return e;
+}
+
+template <int TX, int TY, int NS, bool VAR>
+struct SweepShape {
+    static constexpr int H = 4 * NS;
+    static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
+    static constexpr int R = RX * RY;
+    static constexpr int PLANES = VAR ? 11 : 3; // x, b, inv (+ 8 off-diagonals)
+    static constexpr size_t smem = (size_t)PLANES * R * sizeof(double);
+};
+
+template <int TX, int TY, int NS, bool VAR>
+__global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__ b,
+                                               const double* __restrict__ inv,
+                                               const double* __restrict__ xin,
+                                               double* __restrict__ xout,
+                                               const double* __restrict__ ec, int forward,
+                                               int zero_init)
+{
+    using S = SweepShape<TX, TY, NS, VAR>;
+    constexpr int H = S::H, RX = S::RX, RY = S::RY, R = S::R;
+    constexpr int P = 4 * NS;
+    extern __shared__ double sm[];
+    double* xs = sm;
+    double* bs = xs + R;
+    double* iv = bs + R;
+    double* cs = iv + R; // VAR: plane p holds entry d = p < 4 ? p : p + 1
+
+    const int nx = A.nx;
+    const long long n = (long long)nx * nx;
+    const int nxc = (nx - 1) / 2;
+    const int tx0 = blockIdx.x * TX, ty0 = blockIdx.y * TY;
+    const int ox = tx0 - H, oy = ty0 - H;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+
+    // ---- stage the region: every copy in flight before the first wait
+    for (int ly = ty; ly < RY; ly += 8) {
+        const int gy = oy + ly;
+        const bool rowin = gy >= 0 && gy < nx;
+        for (int lx = tx; lx < RX; lx += 32) {
+            const int gx = ox + lx;
+            const int l = ly * RX + lx;
+            if (rowin && gx >= 0 && gx < nx) {
+                const long long i = (long long)gy * nx + gx;
+                if (zero_init) xs[l] = 0.0;
+                else cp_async8(xs + l, xin + i);
+                cp_async8(bs + l, b + i);
+                cp_async8(iv + l, inv + i);
+                if (VAR) {
+#pragma unroll
+                    for (int p = 0; p < 8; ++p) cp_async8(cs + p * R + l, A.coef + (p < 4 ? p : p + 1) * n + i);
+                }
+            } else {
+                xs[l] = 0.0;
+                bs[l] = 0.0;
+                iv[l] = 0.0;
+                if (VAR) {
+#pragma unroll
+                    for (int p = 0; p < 8; ++p) cs[p * R + l] = 0.0;
+                }
+            }
+        }
+    }
+    cp_async_wait_all();
+    if (ec) {
+        __syncthreads();
+        for (int ly = ty; ly < RY; ly += 8) {
+            const int gy = oy + ly;
+            if (gy < 0 || gy >= nx) continue;
+            for (int lx = tx; lx < RX; lx += 32) {
+                const int gx = ox + lx;
+                if (gx < 0 || gx >= nx) continue;
+                xs[ly * RX + lx] = xs[ly * RX + lx] + prolong_at2(ec, nxc, gx, gy); // x += P ec
+            }
+        }
+    }
+    __syncthreads();
+
+#pragma unroll 1
+    for (int q = 0; q < P; ++q) {
+        const int pc = q & 3;
+        const int c = forward ? pc : 3 - pc;
+        const int cx = c & 1, cy = c >> 1;
+        const int g = P - 1 - q;
+        const int lox = max(tx0 - g, 0), hix = min(tx0 + TX + g, nx);
+        const int loy = max(ty0 - g, 0), hiy = min(ty0 + TY + g, nx);
+        const int gx0 = lox + ((lox & 1) ^ cx);
+        const int gy0 = loy + ((loy & 1) ^ cy);
+        for (int gy = gy0 + 2 * ty; gy < hiy; gy += 16) {
+            for (int gx = gx0 + 2 * tx; gx < hix; gx += 64) {
+                const int l = (gy - oy) * RX + (gx - ox);
+                double s = bs[l];
+#pragma unroll
+                for (int d = 0; d < 9; ++d) {
+                    if (d == 4) continue;
+                    const double a = VAR ? cs[(d < 4 ? d : d - 1) * R + l] : A.c[d];
+                    s -= a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
+                }
+                xs[l] = s * iv[l];
+            }
+        }
+        __syncthreads();
+    }
+
+    for (int ly = ty; ly < TY; ly += 8) {
+        const int gy = ty0 + ly;
+        if (gy >= nx) break;
+        for (int lx = tx; lx < TX; lx += 32) {
+            const int gx = tx0 + lx;
+            if (gx < nx) xout[(long long)gy * nx + gx] = xs[(ly + H) * RX + lx + H];
+        }
+    }
+}
+
+// r = b - A x on the fine tile of a CX x CY coarse tile, then R = P^T.
+template <int CX, int CY, bool VAR>
+__global__ void __launch_bounds__(256) k_resid_restrict(Op9 A, const double* __restrict__ b,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ bc,
+                                                        double* __restrict__ xc)
+{
+    constexpr int FX = 2 * CX + 1, FY = 2 * CY + 1; // fine nodes feeding the coarse tile
+    constexpr int XX = FX + 2, XY = FY + 2;         // plus the stencil halo
+    constexpr int F = FX * FY;
+    extern __shared__ double sm[];
+    double* xs = sm;            // XX*XY
+    double* rs = xs + XX * XY;  // F (b on entry, r after)
+    double* cf = rs + F;        // VAR: 9*F coefficients
+    const int nx = A.nx;
+    const long long n = (long long)nx * nx;
+    const int nxc = (nx - 1) / 2;
+    const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY;
+    const int fx0 = 2 * cx0, fy0 = 2 * cy0;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int ly = ty; ly < XY; ly += 8) {
+        const int gy = fy0 - 1 + ly;
+        for (int lx = tx; lx < XX; lx += 32) {
+            const int gx = fx0 - 1 + lx;
+            if (gx >= 0 && gx < nx && gy >= 0 && gy < nx) cp_async8(xs + ly * XX + lx, x + (long long)gy * nx + gx);
+            else xs[ly * XX + lx] = 0.0;
+        }
+    }
+    for (int ly = ty; ly < FY; ly += 8) {
+        const int gy = fy0 + ly;
+        for (int lx = tx; lx < FX; lx += 32) {
+            const int gx = fx0 + lx;
+            const int l = ly * FX + lx;
+            if (gx < nx && gy < nx) {
+                const long long i = (long long)gy * nx + gx;
+                cp_async8(rs + l, b + i);
+                if (VAR) {
+#pragma unroll
+                    for (int d = 0; d < 9; ++d) cp_async8(cf + d * F + l, A.coef + d * n + i);
+                }
+            } else {
+                rs[l] = 0.0;
+                if (VAR) {
+#pragma unroll
+                    for (int d = 0; d < 9; ++d) cf[d * F + l] = 0.0;
+                }
+            }
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    for (int ly = ty; ly < FY; ly += 8) {
+        const int gy = fy0 + ly;
+        for (int lx = tx; lx < FX; lx += 32) {
+            const int gx = fx0 + lx;
+            const int l = ly * FX + lx;
+            if (gx < nx && gy < nx) {
+                const int lxs = (ly + 1) * XX + lx + 1;
+                double s = 0.0; // multigrid.cpp:120-121: r = A x; r = rhs - r
+#pragma unroll
+                for (int d = 0; d < 9; ++d) {
+                    double a = VAR ? cf[d * F + l] : A.c[d];
+                    if (d == 4 && A.diag) a += A.diag[(long long)gy * nx + gx];
+                    s += a * xs[lxs + (d / 3 - 1) * XX + (d % 3 - 1)];
+                }
+                rs[l] = rs[l] - s;
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = ty; j < CY; j += 8) {
+        const int cy = cy0 + j;
+        for (int k = tx; k < CX; k += 32) {
+            const int cx = cx0 + k;
+            if (cx >= nxc || cy >= nxc) continue;
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double wy = (a == 1) ? 1.0 : 0.5;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double wx = (c == 1) ? 1.0 : 0.5;
+                    s += (wx * wy) * rs[(2 * j + a) * FX + 2 * k + c];
+                }
+            }
+            const long long I = (long long)cy * nxc + cx;
+            bc[I] = s;
+            if (xc) xc[I] = 0.0;
+        }
+    }
+}
+
+__global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long long fds)
+{
+    const long long n = (long long)A.nx * A.nx;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int bt = blockIdx.y;
+    double a = A.coef ? A.coef[bt * fcs + 4 * n + i] : A.c[4];
+    if (A.diag) a += A.diag[bt * fds + i];
+    inv[bt * n + i] = 1.0 / a;
+}
+
+template <int TX, int TY, int NS, bool VAR>
+void sweep_go(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
+              double* xo, bool forward, bool zero_init, const double* ec)
+{
+    constexpr size_t smem = SweepShape<TX, TY, NS, VAR>::smem;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_sweep<TX, TY, NS, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
+    note_launch();
+    k_sweep<TX, TY, NS, VAR><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
+                                                      zero_init ? 1 : 0);
+}
+
+template <int TX, int TY, int NS>
+void sweep_pick_var(cudaStream_t s, const Op9& A, const double* b, const double* inv,
+                    const double* x, double* xo, bool forward, bool zero_init, const double* ec)
+{
+    if (A.coef) sweep_go<TX, TY, NS, true>(s, A, b, inv, x, xo, forward, zero_init, ec);
+    else sweep_go<TX, TY, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec);
+}
+
+} // namespace
+
+int g_sweep_tile = -1; // tuning override: -1 auto, else tile id (see launch_sweep_tiled)
+int g_sweep_fuse = 1;  // sweeps fused per launch
+
+void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
+                     long long fds)
+{
+    const long long n = (long long)A.nx * A.nx;
+    note_launch();
+    k_inv_diag<<<dim3((unsigned)((n + 255) / 256), batch), 256, 0, s>>>(A, inv, fcs, fds);
+}
+
+void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
+                        const double* x, double* xo, bool forward, bool zero_init,
+                        const double* ec, int ns)
+{
+    int id = g_sweep_tile;
+    if (id < 0) id = A.nx >= 1000 ? 1 : (A.nx >= 500 ? 2 : 3);
+    if (A.coef && id == 0) id = 1; // 64x32 variable tiles exceed shared memory
+    if (ns == 2) {
+        switch (id) {
+        case 0: sweep_go<64, 32, 2, false>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+        case 1: sweep_pick_var<32, 32, 2>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+        case 2: sweep_pick_var<32, 16, 2>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+        default: sweep_pick_var<16, 16, 2>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+        }
+        return;
+    }
+    switch (id) {
+    case 0: sweep_go<64, 32, 1, false>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    case 1: sweep_pick_var<32, 32, 1>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    case 2: sweep_pick_var<32, 16, 1>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    default: sweep_pick_var<16, 16, 1>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    }
+}
+
+void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, const double* x,
+                                 double* bc, double* xc)
+{
+    constexpr int CX = 32, CY = 8;
+    constexpr int F = (2 * CX + 1) * (2 * CY + 1);
+    constexpr int XS = (2 * CX + 3) * (2 * CY + 3);
+    const int nxc = (A.nx - 1) / 2;
+    dim3 grid((nxc + CX - 1) / CX, (nxc + CY - 1) / CY);
+    note_launch();
+    if (A.coef) {
+        constexpr size_t smem = (size_t)(XS + 10 * F) * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_resid_restrict<CX, CY, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        k_resid_restrict<CX, CY, true><<<grid, 256, smem, s>>>(A, b, x, bc, xc);
+    } else {
+        constexpr size_t smem = (size_t)(XS + F) * sizeof(double);
+        k_resid_restrict<CX, CY, false><<<grid, 256, smem, s>>>(A, b, x, bc, xc);
+    }
+}
+
+} // namespace ocb

@@ -38,6 +38,18 @@ void launch_gs_sweep(cudaStream_t s, const Op9& A, const double* b, const double
 // also zeroes the coarse iterate xc (if non-null).
 void launch_residual_restrict(cudaStream_t s, const Op9& A, const double* b, const double* x,
                               double* bc, double* xc);
+// k_mg_tiled.cu: the same two operations, tiled for the large levels (>= 8):
+// `ns` fused sweeps per launch (1 or 2); g_sweep_tile overrides the tile choice.
+extern int g_sweep_tile;
+extern int g_sweep_fuse; // sweeps per launch in the V-cycle (1 or 2)
+// inv = 1 / diag(A) precomputed per level (launch_inv_diag).
+void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
+                        const double* x, double* xo, bool forward, bool zero_init,
+                        const double* ec, int ns);
+void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
+                     long long fds);
+void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, const double* x,
+                                 double* bc, double* xc);
 // x += P ec
 void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x);
 // partial sums of |b - A x|^2 into part[kRedBlocks]

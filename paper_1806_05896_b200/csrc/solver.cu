@@ -171,6 +171,9 @@ void Hierarchy::allocate(int level, int batch)
         b_[k].resize(n);
     }
     xb_[0].resize((size_t)level_n(0));
+    inv_.clear();
+    inv_.resize(K_ + 1);
+    for (int k = 0; k < kb_; ++k) inv_[k].resize((size_t)level_n(k) * batch);
     lu_.resize(81 * (size_t)batch);
     perm_.resize(9 * (size_t)batch);
     part_.resize(kRedBlocks);
@@ -207,7 +210,18 @@ void Hierarchy::build(Ctx& c, const Op9& fine, long long fcs, long long fds)
                    9 * level_n(k + 1));
     }
     launch_coarse_lu(c.stream, coef_[K_].get(), lu_.get(), perm_.get(), batch_);
+    build_inv(c);
     launch_check("multigrid build");
+}
+
+void Hierarchy::build_inv(Ctx& c)
+{
+    for (int k = 0; k < kb_; ++k) {
+        const Op9 a = level_op(k, 0);
+        const long long cs = k == 0 ? fine_coef_stride_ : 9 * level_n(k);
+        const long long ds = k == 0 ? fine_diag_stride_ : 0;
+        launch_inv_diag(c.stream, a, inv_[k].get(), batch_, cs, ds);
+    }
 }
 
 void Hierarchy::build_rediscretized(Ctx& c, const Op9& fine, const std::vector<const double*>& base)
@@ -234,6 +248,7 @@ void Hierarchy::build_rediscretized(Ctx& c, const Op9& fine, const std::vector<c
         rem.coef = rem_[k + 1].get();
     }
     launch_coarse_lu(c.stream, coef_[K_].get(), lu_.get(), perm_.get(), 1);
+    build_inv(c);
     launch_check("multigrid build (rediscretised)");
 }
 
@@ -263,7 +278,10 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
     const Op9 A = level_op(k, bt);
     double* Abuf = xout;
     double* Bbuf = xb_[k].get();
-    const int S = p.pre + p.post;
+    // sweeps are fused g_sweep_fuse at a time (same colour-pass sequence)
+    const int F = g_sweep_fuse < 1 ? 1 : (g_sweep_fuse > 2 ? 2 : g_sweep_fuse);
+    const int Lpre = (p.pre + F - 1) / F, Lpost = (p.post + F - 1) / F;
+    const int S = Lpre + Lpost; // out-of-place launches; the last one must land in xout
     auto outbuf = [&](int s) { return ((S - s) % 2 == 0) ? Abuf : Bbuf; };
     const double* cur = zero_in ? nullptr : xout;
     const long long n = level_n(k);
@@ -272,37 +290,42 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
         cur = Bbuf;
     }
     int s = 0;
-    for (int i = 0; i < p.pre; ++i) {
+    for (int done = 0; done < p.pre;) {
+        const int ns = std::min(F, p.pre - done);
         ++s;
         double* out = outbuf(s);
         {
-            ProfScope ps(c, k == 0 ? kProfSweep : kProfCats);
-            launch_gs_sweep(c.stream, A, b, cur, out, true, cur == nullptr, nullptr);
+            ProfScope ps(c, (k == 0 && ns == 1) ? kProfSweep : kProfCats);
+            launch_sweep_tiled(c.stream, A, b, inv_at(k, bt), cur, out, true, cur == nullptr,
+                               nullptr, ns);
         }
         cur = out;
+        done += ns;
     }
     if (!cur) {
         double* out = outbuf(s);
         launch_fill(c.stream, out, 0.0, n);
         cur = out;
     }
-    launch_residual_restrict(c.stream, A, b, cur, b_[k + 1].get(), xa_[k + 1].get());
+    launch_resid_restrict_tiled(c.stream, A, b, cur, b_[k + 1].get(), xa_[k + 1].get());
     vcycle(c, k + 1, b_[k + 1].get(), xa_[k + 1].get(), true, p, bt, flags);
     const double* ec = xa_[k + 1].get();
     if (p.post == 0) {
         launch_prolong_add(c.stream, nx_[k], ec, const_cast<double*>(cur));
         return;
     }
-    for (int i = 0; i < p.post; ++i) {
+    for (int done = 0; done < p.post;) {
+        const int ns = std::min(F, p.post - done);
         ++s;
         double* out = outbuf(s);
         {
-            // the first post sweep also applies the prolongation (fused); count
-            // it as a sweep only when it is a plain one
-            ProfScope ps(c, (k == 0 && i > 0) ? kProfSweep : kProfCats);
-            launch_gs_sweep(c.stream, A, b, cur, out, false, false, i == 0 ? ec : nullptr);
+            // the first post launch also applies the prolongation (fused)
+            ProfScope ps(c, (k == 0 && done > 0 && ns == 1) ? kProfSweep : kProfCats);
+            launch_sweep_tiled(c.stream, A, b, inv_at(k, bt), cur, out, false, false,
+                               done == 0 ? ec : nullptr, ns);
         }
         cur = out;
+        done += ns;
     }
 }
 
@@ -336,8 +359,11 @@ void Hierarchy::solve(Ctx& c, const double* b, double* x, const MgParams& p, int
 void Hierarchy::smooth(Ctx& c, const double* b, double* x, bool forward, int bt)
 {
     const Op9 A = level_op(0, bt);
-    launch_gs_sweep(c.stream, A, b, x, xb_[0].get(), forward, false, nullptr);
+    DVec inv((size_t)level_n(0));
+    launch_inv_diag(c.stream, A, inv.get(), 1, 0, 0);
+    launch_sweep_tiled(c.stream, A, b, inv.get(), x, xb_[0].get(), forward, false, nullptr, 1);
     launch_copy(c.stream, xb_[0].get(), x, level_n(0));
+    c.sync();
     launch_check("smoothing sweep");
 }
 

@@ -153,6 +153,8 @@ private:
     void vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_in, const MgParams& p,
                 int bt, int* flags);
     BottomArgs bottom_args(int kfrom, int bt) const;
+    void build_inv(Ctx& c);
+    const double* inv_at(int k, int bt) const { return inv_[k].get() + (size_t)bt * level_n(k); }
 
     int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1;
     bool cluster_ = false;  // bottom levels run in the 16-CTA cluster kernel
@@ -163,6 +165,7 @@ private:
     std::vector<DVec> rem_;         // rediscretised remainder chain, k >= 1 (batch 1)
     DVec remfine_;                  // fine remainder fine - base(level), 9 arrays
     std::vector<DVec> xa_, xb_, b_; // per level work (k >= 1); xb_[0] fine scratch
+    std::vector<DVec> inv_;         // 1/diag per tiled level (k < kb_), batch-strided
     DVec lu_;
     DevArray<int> perm_;
     DVec part_, state_;
