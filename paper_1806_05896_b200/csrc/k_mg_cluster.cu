@@ -2,27 +2,36 @@
 //
 // Levels <= 7 of a V-cycle are latency-bound: a level-7 colour pass touches
 // 4K nodes, far too little work to amortise a kernel launch, and the
-// reference's V-cycle runs 44 such dependent phases per level
-// (multigrid.cpp:111-132). This kernel keeps the whole bottom of the
-// hierarchy on chip in one thread-block cluster of kCS CTAs:
-//   * "slab" levels (7 and 6): CTAs 1..kCS-1 each own a band of rows; their
-//     x, b, r and the 9 coefficient arrays live in that CTA's shared memory.
-//     A node on a band edge is also stored (remote DSM store) into the
-//     neighbouring CTA's halo row as soon as it is updated, so every colour
-//     pass reads only local shared memory; passes are separated by cluster
-//     barriers (release/acquire makes the pushed halos visible);
-//   * levels <= 5: CTA 0 alone holds everything in its shared memory and runs
-//     with block barriers, then the 9x9 LU solve at level 2.
-// Geometry is compile-time (template on the top level), so thread->node maps
-// are shifts and masks. Semantics match the device V-cycle elsewhere: 4-colour
-// symmetric Gauss-Seidel (forward 0..3 pre, backward 3..0 post), R = P^T,
-// bilinear prolongation, zero coarse initial guesses and, when this kernel is
-// the whole solve, `cycles` V-cycles with the ||r|| > 10 ||r_prev|| check of
-// MgHierarchy::solve (multigrid.cpp:141-157).
+// reference's V-cycle runs 44 dependent phases per level
+// (multigrid.cpp:111-132). This kernel keeps the bottom of the hierarchy on
+// chip in one thread-block cluster of 16 CTAs x 256 threads:
+//   * slab levels (the top level TOP = 7 or 6, and level 6 below a level-7
+//     top): CTA w owns rows [RP*w, RP*w+RP). Thread t owns one node of EACH
+//     colour (same position in the four colour sub-grids), so every colour
+//     pass keeps all warps busy and no warp burns issue slots idling; the top
+//     level keeps the 4 nodes' 9 coefficients, 1/a_ii and b in registers.
+//     x is stored colour-planar with one halo row above and below, so every
+//     neighbour read is a conflict-free shared-memory load.
+//   * halo exchange is dataflow, not a cluster barrier: after a colour pass a
+//     band-edge node st.async's its new value into the neighbour CTA's halo
+//     row, completing bytes on that CTA's per-colour mbarrier; a CTA waits on
+//     its mbarrier only before a pass that reads that colour of a halo row.
+//     (Only the first band row, colours 0/1, feeds the CTA above; only the
+//     last, colours 2/3, feeds the CTA below.) Prolongation of halo rows is
+//     recomputed locally from the same parents (bit-identical), so there are
+//     no exchange events outside the smoothing passes;
+//   * levels <= 5 run in CTA 0 alone (planar shared memory, block barriers),
+//     ending with the 9x9 LU solve at level 2 (factor held in shared memory).
+// Semantics match the tiled V-cycle levels: 4-colour symmetric Gauss-Seidel
+// (forward colours 0..3 pre, backward 3..0 post), R = P^T restriction of the
+// residual, bilinear prolongation, zero coarse initial guesses and, when this
+// kernel is the whole solve, `cycles` V-cycles with the ||r|| > 10 ||r_prev||
+// check of MgHierarchy::solve (multigrid.cpp:141-157).
 #include "kernels.hpp"
 
 #include <cooperative_groups.h>
 
+#include <cstdint>
 #include <stdexcept>
 
 namespace cg = cooperative_groups;
@@ -31,188 +40,273 @@ namespace ocb {
 
 namespace {
 
-constexpr int kCS = 16;          // CTAs per cluster (non-portable size)
-constexpr int kW = kCS - 1;      // worker CTAs owning slab rows
-constexpr int kCT = 1024;        // threads per CTA
+constexpr int kCS = 16;  // CTAs per cluster (non-portable size)
+constexpr int kCT = 256; // threads per CTA
 
-template <int TOP>
-struct Geo {
-    static constexpr int NLEV = TOP - 1;                 // levels TOP..2
-    static constexpr int nx(int k) { return (1 << (TOP - k)) - 1; }
-    static constexpr bool slab(int k) { return nx(k) > 31; }
-    static constexpr int rp(int k) { return (nx(k) + kW - 1) / kW; }
-    static constexpr int cnt(int k) { return slab(k) ? rp(k) * nx(k) : nx(k) * nx(k); }
-    // worker layout per slab level: coef 9*cnt, x, b, r, inv-diag (cnt each), halo above/below
-    static constexpr int wsize(int k) { return 13 * cnt(k) + 2 * nx(k); }
-    static constexpr int woff(int k) { return k == 0 ? 0 : woff(k - 1) + (slab(k - 1) ? wsize(k - 1) : 0); }
-    // CTA-0 layout per coarse level: coef 9*cnt, x, b, inv-diag; one residual scratch at the end
-    static constexpr int csize(int k) { return 12 * cnt(k); }
-    // threads working a CTA-0 level: the colour lattice rounded up to whole warps
-    static constexpr int c0threads(int k) { return ((((nx(k) + 1) / 2) * ((nx(k) + 1) / 2) + 31) / 32) * 32; }
-    static constexpr int coff(int k) { return k == 0 ? 0 : coff(k - 1) + (slab(k - 1) ? 0 : csize(k - 1)); }
-    static constexpr int first_c0() { return slab(0) ? (slab(1) ? 2 : 1) : 0; }
-    static constexpr int cscratch() { return coff(NLEV - 1) + csize(NLEV - 1); }
-    static constexpr int wtotal() { return woff(NLEV - 1) + (slab(NLEV - 1) ? wsize(NLEV - 1) : 0); }
-    static constexpr int ctotal() { return cscratch() + cnt(first_c0()); }
-    static constexpr int total() { return wtotal() > ctotal() ? wtotal() : ctotal(); }
+// --------------------------------------------------- mbarrier / DSM primitives
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
+{
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n .reg .pred p;\n"
+                     " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done)
+                     : "r"(bar), "r"(parity)
+                     : "memory");
+    }
+}
+
+__device__ __forceinline__ void st_async(uint32_t raddr, double v, uint32_t rbar)
+{
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+
+// ------------------------------------------------------------- geometry
+__host__ __device__ constexpr int fl2(int v) { return (v - (((v % 2) + 2) % 2)) / 2; } // floor(v / 2)
+
+// Colour-planar layouts: plane (gx & 1) + 2 (row & 1) holds the nodes of one
+// colour; rows of a plane are padded by one leading column (and the CTA-0
+// levels by one leading row) that stay zero, so a neighbour outside the
+// domain reads 0 and every neighbour of a thread's colour-c node is
+// x[q + nb(c, dx, dy)] with a compile-time offset and q = rr * SX + cc.
+template <int NX_, int RP_>
+struct SlabG {
+    static constexpr int NX = NX_, RP = RP_;
+    static constexpr int WX = (NX + 1) / 2;     // columns per colour row
+    static constexpr int SX = WX + 1;           // padded row stride
+    static constexpr int RH = RP / 2;           // colour rows per band
+    static constexpr int PS = (RH + 1) * SX;    // plane size (incl. the halo rows)
+    static constexpr int XS = 4 * PS;           // planar x with halos
+    static constexpr int GROUP = RH * WX;       // threads owning nodes (one per colour)
+    static constexpr int RS = RP * NX;          // row-major residual of own rows
+    static_assert(RP % 2 == 0, "even row bands keep the colour parity per CTA");
+    static_assert(GROUP <= kCT, "one node per colour per thread");
+    static_assert(2 * NX <= kCT, "one halo node per thread");
+    // planar index of (gx, local row lr); lr = gy - r0 + 1 in [0, RP + 1]
+    __host__ __device__ static constexpr int xi(int gx, int lr)
+    {
+        return ((gx & 1) + 2 * (lr & 1)) * PS + (lr >> 1) * SX + fl2(gx) + 1;
+    }
+    // offset of neighbour (dx, dy) of the colour-c node at (cc, rr), relative to q
+    __host__ __device__ static constexpr int nb(int c, int dx, int dy)
+    {
+        return xi((c & 1) + dx, (c >> 1) + 1 + dy);
+    }
+    // bytes of one colour segment of a row (colours 0, 2: even gx; 1, 3: odd gx)
+    __device__ static __forceinline__ uint32_t seg_bytes(int c) { return 8u * ((c & 1) ? NX / 2 : (NX + 1) / 2); }
 };
 
-// ------------------------------------------------------------ slab levels
-template <int NX, int RP>
-struct Slab {
-    static constexpr int CNT = RP * NX;
-    double* coef;   // [9][CNT]
-    double* x;      // [CNT]
+template <int NX>
+struct FullG { // CTA-0 level: planar x, b, inv, r, coefficients; padded, no halos
+    static constexpr int WX = (NX + 1) / 2;
+    static constexpr int SX = WX + 1;
+    static constexpr int PS = (WX + 1) * SX;
+    static constexpr int S = 4 * PS;
+    static_assert(WX * WX <= kCT, "one node per colour per thread");
+    __host__ __device__ static constexpr int xi(int gx, int gy)
+    {
+        return ((gx & 1) + 2 * (gy & 1)) * PS + (fl2(gy) + 1) * SX + fl2(gx) + 1;
+    }
+    __host__ __device__ static constexpr int nb(int c, int dx, int dy) { return xi((c & 1) + dx, (c >> 1) + dy); }
+};
+
+// The four nodes (one per colour c) a thread owns on a slab level:
+// gx = 2 cc + (c & 1), gy = r0 + 2 rr + (c >> 1), local row lr = gy - r0 + 1.
+template <class G>
+struct Own {
+    int cc, rr, r0, q;
+    bool thr; // thread owns nodes on this level
+    __device__ explicit Own(int w)
+    {
+        const int t = threadIdx.x;
+        thr = t < G::GROUP;
+        rr = t / G::WX;
+        cc = t - rr * G::WX;
+        r0 = G::RP * w;
+        q = rr * G::SX + cc;
+    }
+    __device__ __forceinline__ int gx(int c) const { return 2 * cc + (c & 1); }
+    __device__ __forceinline__ int gy(int c) const { return r0 + 2 * rr + (c >> 1); }
+    __device__ __forceinline__ int lr(int c) const { return 2 * rr + (c >> 1) + 1; }
+    __device__ __forceinline__ bool valid(int c) const { return thr && gx(c) < G::NX && gy(c) < G::NX; }
+    __device__ __forceinline__ int me(int c) const { return q + G::nb(c, 0, 0); }
+    __device__ __forceinline__ int slot(int c) const { return c * G::GROUP + threadIdx.x; }
+};
+
+// x(gx+dx, gy+dy) of the colour-c node from the local planar band (own rows +
+// halo rows; outside the domain the zero padding / never-written slots read 0)
+template <class G>
+__device__ __forceinline__ double xnb(const double* xs, const Own<G>& o, int c, int dx, int dy)
+{
+    return xs[o.q + G::nb(c, dx, dy)];
+}
+
+// Halo exchange state of one slab level. mbarrier c of a CTA counts the bytes
+// of colour c arriving in its halo rows: colours 0/1 from the CTA below (its
+// first row), colours 2/3 from the CTA above (its last row). Bit c of `pend`
+// marks an exchange of colour c not yet consumed, bit c of `par` the parity of
+// the next phase of barrier c. At most one exchange per colour is ever in
+// flight: a neighbour's next colour-c pass depends on values this CTA sends
+// only after consuming the previous one (and every V-cycle phase boundary
+// consumes all exchanges), so parity waits cannot alias.
+template <class G>
+struct Halo {
+    uint32_t bar; // local mbarriers (4 x 8 bytes)
+    uint32_t xs;  // local planar x (shared address)
+    int w;
+    unsigned pend, par;
+
+    __device__ void setup(uint64_t* bars, double* x, int rank)
+    {
+        bar = saddr(bars);
+        xs = saddr(x);
+        w = rank;
+        pend = par = 0u;
+    }
+    __device__ bool has_up() const { return w > 0; }
+    __device__ bool has_dn() const { return G::RP * (w + 1) < G::NX; }
+    // thread 0: init and arm phase 0 of the four barriers
+    __device__ void init_barriers() const
+    {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            mbar_init(bar + 8 * c, 1);
+            mbar_expect(bar + 8 * c, G::seg_bytes(c));
+        }
+    }
+    __device__ __forceinline__ void ensure(int c)
+    {
+        if (!((pend >> c) & 1u)) return;
+        pend &= ~(1u << c);
+        if (!(c < 2 ? has_dn() : has_up())) return;
+        mbar_wait(bar + 8 * c, (par >> c) & 1u);
+        par ^= 1u << c;
+        if (threadIdx.x == 0) mbar_expect(bar + 8 * c, G::seg_bytes(c));
+    }
+    __device__ __forceinline__ void ensure_all()
+    {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ensure(c);
+    }
+    // after the CTA barrier of a colour-c pass: send the band-edge value
+    __device__ __forceinline__ void push(const Own<G>& o, double v, int c) const
+    {
+        if (c < 2 && o.rr == 0 && has_up())
+            st_async(mapa(xs + 8u * G::xi(o.gx(c), G::RP + 1), (uint32_t)(w - 1)), v,
+                     mapa(bar + 8 * c, (uint32_t)(w - 1)));
+        if (c >= 2 && o.rr == G::RH - 1 && has_dn())
+            st_async(mapa(xs + 8u * G::xi(o.gx(c), 0), (uint32_t)(w + 1)), v,
+                     mapa(bar + 8 * c, (uint32_t)(w + 1)));
+    }
+    __device__ __forceinline__ void passed(int c) { pend |= 1u << c; }
+};
+
+// One symmetric-colour GS sweep on a slab level. upd(c) returns the new value
+// of the thread's colour-c node.
+template <bool FWD, class G, typename U>
+__device__ __forceinline__ void slab_sweep(double* xs, Halo<G>& H, const Own<G>& o, const U& upd)
+{
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int c = FWD ? p : 3 - p;
+        if (c < 2) { // first-row nodes read the upper halo (colours 2, 3)
+            H.ensure(2);
+            H.ensure(3);
+        } else { // last-row nodes read the lower halo (colours 0, 1)
+            H.ensure(0);
+            H.ensure(1);
+        }
+        const bool act = o.valid(c);
+        double v = 0.0;
+        if (act) {
+            v = upd(c);
+            xs[o.me(c)] = v;
+        }
+        __syncthreads(); // CTA-local visibility; every halo read of this pass is done
+        if (act) H.push(o, v, c);
+        H.passed(c);
+    }
+}
+
+// ----------------------------------------------------------- CTA-0 levels
+template <int NX>
+struct C0Level {
+    double* coef; // [9][S] planar
+    double* x;    // [S]
     double* b;
+    double* inv;
     double* r;
-    double* inv;    // 1 / a_ii
-    double* ha;     // halo row above (row r0-1), NX
-    double* hb;     // halo row below (row r1), NX
-    int w, r0, r1;  // worker index, own rows [r0, r1)
-
-    __device__ Slab(double* base, unsigned rank)
-    {
-        coef = base;
-        x = coef + 9 * CNT;
-        b = x + CNT;
-        r = b + CNT;
-        inv = r + CNT;
-        ha = inv + CNT;
-        hb = ha + NX;
-        w = (int)rank - 1;
-        r0 = min(w * RP, NX); // trailing workers may own no rows
-        r1 = min(r0 + RP, NX);
-        if (w < 0) r0 = r1 = 0;
-    }
-    __device__ __forceinline__ double xat(int jx, int jy) const
-    {
-        if (jy < r0) return ha[jx];
-        if (jy >= r1) return hb[jx];
-        return x[(jy - r0) * NX + jx];
-    }
 };
 
-// push an updated edge-row node into the neighbours' halos
-template <int NX, int RP>
-__device__ __forceinline__ void push_halo(cg::cluster_group& cl, const Slab<NX, RP>& s, int gx,
-                                          int gy, double v, int base_off, double* smem)
+template <bool FWD, int NX>
+__device__ void c0_sweep(const C0Level<NX>& L)
 {
-    constexpr int HA = 13 * Slab<NX, RP>::CNT; // offset of ha in a slab
-    if (gy == s.r0 && s.w > 0) {
-        double* dst = cl.map_shared_rank(smem + base_off + HA + NX, (unsigned)s.w); // hb of w-1
-        dst[gx] = v;
-    }
-    if (gy == s.r1 - 1 && s.r1 < NX) {
-        double* dst = cl.map_shared_rank(smem + base_off + HA, (unsigned)(s.w + 2)); // ha of w+1
-        dst[gx] = v;
-    }
-}
-
-template <int NX, int RP>
-__device__ void slab_sweep(cg::cluster_group& cl, const Slab<NX, RP>& s, bool forward, int off,
-                           double* smem)
-{
-    constexpr int CNT = Slab<NX, RP>::CNT;
-    for (int p = 0; p < 4; ++p) {
-        const int col = forward ? p : 3 - p;
-        const int cx = col & 1, cy = col >> 1;
-        if (s.w >= 0) {
-            const int y0 = s.r0 + (((s.r0 & 1) != cy) ? 1 : 0);
-            const int gx = cx + 2 * (threadIdx.x & 63);
-            const int gy = y0 + 2 * (threadIdx.x >> 6);
-            if (gx < NX && gy < s.r1) {
-                const int l = (gy - s.r0) * NX + gx;
-                double acc = s.b[l];
+    using G = FullG<NX>;
+    const int t = threadIdx.x;
+    const int rr = t / G::WX, cc = t - rr * G::WX;
+    const int q = rr * G::SX + cc;
+    const bool thr = t < G::WX * G::WX;
 #pragma unroll
-                for (int d = 0; d < 9; ++d) {
-                    if (d == 4) continue;
-                    const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
-                    if (jx < 0 || jx >= NX || jy < 0 || jy >= NX) continue;
-                    acc -= s.coef[d * CNT + l] * s.xat(jx, jy);
-                }
-                const double v = acc * s.inv[l];
-                s.x[l] = v;
-                push_halo(cl, s, gx, gy, v, off, smem);
-            }
-        }
-        cl.sync();
-    }
-}
-
-template <int NX, int RP>
-__device__ void slab_residual(const Slab<NX, RP>& s)
-{
-    constexpr int CNT = Slab<NX, RP>::CNT;
-    if (s.w < 0) return;
-    for (int idx = threadIdx.x; idx < CNT; idx += blockDim.x) {
-        const int ly = idx / NX, gx = idx - ly * NX, gy = s.r0 + ly;
-        if (gy >= s.r1) continue;
-        double acc = 0.0;
-#pragma unroll
-        for (int d = 0; d < 9; ++d) {
-            const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
-            if (jx < 0 || jx >= NX || jy < 0 || jy >= NX) continue;
-            acc += s.coef[d * CNT + idx] * s.xat(jx, jy);
-        }
-        s.r[idx] = s.b[idx] - acc;
-    }
-}
-
-// ------------------------------------------------------------ CTA-0 levels
-// Each CTA-0 level runs on the first T threads (its colour lattice rounded up to
-// warps) and synchronises with a named barrier over exactly those threads, so
-// the small levels do not pay a 32-warp __syncthreads per colour pass.
-__device__ __forceinline__ void nbar(int id, int nthreads)
-{
-    if (nthreads <= 32) __syncwarp();
-    else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-template <int NX, int T, int BAR>
-__device__ void c0_sweep(const double* coef, double* x, const double* b, const double* inv,
-                         bool forward)
-{
-    constexpr int N = NX * NX;
-    constexpr int LX = (NX + 1) / 2;
     for (int p = 0; p < 4; ++p) {
-        const int col = forward ? p : 3 - p;
-        const int cx = col & 1, cy = col >> 1;
-        const int gx = cx + 2 * (threadIdx.x % LX), gy = cy + 2 * (threadIdx.x / LX);
-        if (gx < NX && gy < NX) {
-            const int i = gy * NX + gx;
-            double acc = b[i];
+        const int c = FWD ? p : 3 - p;
+        const int gx = 2 * cc + (c & 1), gy = 2 * rr + (c >> 1);
+        if (thr && gx < NX && gy < NX) {
+            const int me = q + G::nb(c, 0, 0);
+            double s = L.b[me];
 #pragma unroll
             for (int d = 0; d < 9; ++d) {
                 if (d == 4) continue;
-                const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
-                if (jx < 0 || jx >= NX || jy < 0 || jy >= NX) continue;
-                acc -= coef[d * N + i] * x[jy * NX + jx];
+                s -= L.coef[d * G::S + me] * L.x[q + G::nb(c, d % 3 - 1, d / 3 - 1)];
             }
-            x[i] = acc * inv[i];
+            L.x[me] = s * L.inv[me];
         }
-        nbar(BAR, T);
+        __syncthreads();
     }
 }
 
-template <int NX, int T, int BAR>
-__device__ void c0_residual(const double* coef, const double* x, const double* b, double* r)
+template <int NX>
+__device__ void c0_residual(const C0Level<NX>& L)
 {
-    constexpr int N = NX * NX;
-    for (int i = threadIdx.x; i < N; i += T) {
+    using G = FullG<NX>;
+    for (int i = threadIdx.x; i < NX * NX; i += blockDim.x) {
         const int gy = i / NX, gx = i - gy * NX;
-        double acc = 0.0;
+        const int me = G::xi(gx, gy);
+        double s = 0.0;
 #pragma unroll
         for (int d = 0; d < 9; ++d) {
             const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
             if (jx < 0 || jx >= NX || jy < 0 || jy >= NX) continue;
-            acc += coef[d * N + i] * x[jy * NX + jx];
+            s += L.coef[d * G::S + me] * L.x[G::xi(jx, jy)];
         }
-        r[i] = b[i] - acc;
+        L.r[me] = L.b[me] - s;
     }
-    nbar(BAR, T);
+    __syncthreads();
 }
 
-// R = P^T restriction from a fine residual accessor
+// (R r)(cx, cy) with R = P^T: fine nodes 2c, 2c+1, 2c+2 weighted 1/2, 1, 1/2 per axis
 template <typename F>
 __device__ __forceinline__ double restrict_from(const F& fr, int cx, int cy)
 {
@@ -229,103 +323,68 @@ __device__ __forceinline__ double restrict_from(const F& fr, int cx, int cy)
     return s;
 }
 
-// bilinear prolongation value at fine (gx, gy) from a coarse accessor (NXC per side)
+// parents of fine index g on one axis: (i0, w0), (i1, w1); weight 0 = absent
+template <int NXC>
+__device__ __forceinline__ void parents(int g, int& i0, int& i1, double& w0, double& w1)
+{
+    if (g & 1) {
+        i0 = i1 = (g - 1) >> 1;
+        w0 = 1.0;
+        w1 = 0.0;
+    } else {
+        i0 = g / 2 - 1;
+        i1 = g / 2;
+        w0 = i0 >= 0 ? 0.5 : 0.0;
+        w1 = i1 < NXC ? 0.5 : 0.0;
+    }
+}
+
+// (P e)(gx, gy): bilinear interpolation from the coarse level of size NXC
 template <int NXC, typename F>
 __device__ __forceinline__ double prolong_from(const F& cxv, int gx, int gy)
 {
-    int px[2], py[2];
-    double wx[2], wy[2];
-    int nxn = 0, nyn = 0;
-    if (gx & 1) { px[0] = (gx - 1) >> 1; wx[0] = 1.0; nxn = 1; }
-    else {
-        if (gx / 2 - 1 >= 0) { px[nxn] = gx / 2 - 1; wx[nxn++] = 0.5; }
-        if (gx / 2 < NXC) { px[nxn] = gx / 2; wx[nxn++] = 0.5; }
-    }
-    if (gy & 1) { py[0] = (gy - 1) >> 1; wy[0] = 1.0; nyn = 1; }
-    else {
-        if (gy / 2 - 1 >= 0) { py[nyn] = gy / 2 - 1; wy[nyn++] = 0.5; }
-        if (gy / 2 < NXC) { py[nyn] = gy / 2; wy[nyn++] = 0.5; }
-    }
+    int x0, x1, y0, y1;
+    double wx0, wx1, wy0, wy1;
+    parents<NXC>(gx, x0, x1, wx0, wx1);
+    parents<NXC>(gy, y0, y1, wy0, wy1);
     double e = 0.0;
-    for (int a = 0; a < nyn; ++a)
-        for (int b = 0; b < nxn; ++b) e += (wx[b] * wy[a]) * cxv(px[b], py[a]);
+    if (wy0 != 0.0) {
+        if (wx0 != 0.0) e += (wx0 * wy0) * cxv(x0, y0);
+        if (wx1 != 0.0) e += (wx1 * wy0) * cxv(x1, y0);
+    }
+    if (wy1 != 0.0) {
+        if (wx0 != 0.0) e += (wx0 * wy1) * cxv(x0, y1);
+        if (wx1 != 0.0) e += (wx1 * wy1) * cxv(x1, y1);
+    }
     return e;
 }
 
-// load a level operator (materialising constant stencil + diag) rows [r0, r1)
-// into 9 coefficient arrays plus the reciprocal diagonal used by the smoother
-__device__ void load_op(const Op9& A, int nx, int r0, int r1, int cnt, double* coef, double* inv)
+__device__ __forceinline__ double op_entry(const Op9& A, int d, long long n, long long i)
 {
-    const long long n = (long long)nx * nx;
-    for (int idx = threadIdx.x; idx < (r1 - r0) * nx; idx += blockDim.x) {
-        const long long gi = (long long)r0 * nx + idx;
+    double v = A.coef ? __ldg(A.coef + d * n + i) : A.c[d];
+    if (d == 4 && A.diag) v += __ldg(A.diag + i);
+    return v;
+}
+
+// load a CTA-0 level operator into planar shared memory
+template <int NX>
+__device__ void c0_load(const Op9& A, const C0Level<NX>& L)
+{
+    using G = FullG<NX>;
+    const long long n = (long long)NX * NX;
+    for (int i = threadIdx.x; i < G::S; i += blockDim.x) L.x[i] = 0.0; // padding stays zero
+    for (int i = threadIdx.x; i < NX * NX; i += blockDim.x) {
+        const int gy = i / NX, gx = i - gy * NX;
+        const int me = G::xi(gx, gy);
 #pragma unroll
         for (int d = 0; d < 9; ++d) {
-            double v = A.coef ? __ldg(A.coef + d * n + gi) : A.c[d];
-            if (d == 4 && A.diag) v += __ldg(A.diag + gi);
-            coef[d * cnt + idx] = v;
-            if (d == 4) inv[idx] = 1.0 / v;
+            const double v = op_entry(A, d, n, i);
+            L.coef[d * G::S + me] = v;
+            if (d == 4) L.inv[me] = 1.0 / v;
         }
     }
 }
 
-// CTA-0 part of the V-cycle for levels K..NLEV-1 (all <= 31 per side). Runs on
-// threads [0, T_K); callers keep the other threads out.
-template <int TOP, int K>
-struct C0Down {
-    using G = Geo<TOP>;
-    static __device__ void run(double* smem, const BottomArgs& a, int pre, int post)
-    {
-        constexpr int NX = G::nx(K);
-        constexpr int N = NX * NX;
-        constexpr int T = G::c0threads(K);
-        constexpr int BAR = 1 + K; // named barrier per level (0 is __syncthreads)
-        double* coef = smem + G::coff(K);
-        double* x = coef + 9 * N;
-        double* b = x + N;
-        double* inv = b + N;
-        if constexpr (K == G::NLEV - 1) {
-            // level 2: dense 9x9 LU solve (DenseFactor::solve)
-            if (threadIdx.x == 0) {
-                double y[9];
-                for (int i = 0; i < 9; ++i) y[i] = b[a.perm[i]];
-                for (int i = 0; i < 9; ++i)
-                    for (int k2 = 0; k2 < i; ++k2) y[i] -= a.lu[k2 * 9 + i] * y[k2];
-                for (int i = 8; i >= 0; --i) {
-                    for (int k2 = i + 1; k2 < 9; ++k2) y[i] -= a.lu[k2 * 9 + i] * y[k2];
-                    y[i] /= a.lu[i * 9 + i];
-                }
-                for (int i = 0; i < 9; ++i) x[i] = y[i];
-            }
-            __syncwarp();
-        } else {
-            constexpr int NC = G::nx(K + 1);
-            constexpr int TC = G::c0threads(K + 1);
-            double* r = smem + G::cscratch();
-            double* cb = smem + G::coff(K + 1) + 10 * NC * NC;
-            double* cx = smem + G::coff(K + 1) + 9 * NC * NC;
-            for (int s = 0; s < pre; ++s) c0_sweep<NX, T, BAR>(coef, x, b, inv, true);
-            c0_residual<NX, T, BAR>(coef, x, b, r);
-            for (int I = threadIdx.x; I < NC * NC; I += T) {
-                const int cy = I / NC, cxx = I - cy * NC;
-                cb[I] = restrict_from([&](int gx, int gy) { return r[gy * NX + gx]; }, cxx, cy);
-                cx[I] = 0.0;
-            }
-            nbar(BAR, T);
-            if (threadIdx.x < TC) C0Down<TOP, K + 1>::run(smem, a, pre, post);
-            nbar(BAR, T);
-            for (int i = threadIdx.x; i < N; i += T) {
-                const int gy = i / NX, gx = i - gy * NX;
-                x[i] = x[i] + prolong_from<NC>([&](int u, int v) { return cx[v * NC + u]; }, gx, gy);
-            }
-            nbar(BAR, T);
-            for (int s = 0; s < post; ++s) c0_sweep<NX, T, BAR>(coef, x, b, inv, false);
-        }
-    }
-};
-
-// --------------------------------------------------------------- kernel
-// Optional phase timestamps (%globaltimer) of CTAs 0 and 1 for tuning.
 __device__ int g_probe_on = 0;
 __device__ unsigned long long g_tprobe[64];
 __device__ __forceinline__ void probe(unsigned rank, int i)
@@ -337,215 +396,414 @@ __device__ __forceinline__ void probe(unsigned rank, int i)
     }
 }
 
+// CTA-0 V-cycle for levels of size NX, NX/2, ..., 3 (LU at 3x3)
+template <int NX>
+struct C0Cycle {
+    static constexpr int DEPTH = 1 + C0Cycle<NX / 2>::DEPTH;
+    static constexpr size_t doubles() { return 13 * (size_t)FullG<NX>::S + C0Cycle<NX / 2>::doubles(); }
+    __device__ static void layout(double* base, C0Level<NX>& L)
+    {
+        constexpr int S = FullG<NX>::S;
+        L.coef = base;
+        L.x = base + 9 * S;
+        L.b = L.x + S;
+        L.inv = L.b + S;
+        L.r = L.inv + S;
+    }
+    __device__ static void load(double* base, const BottomArgs& a, int k)
+    {
+        C0Level<NX> L;
+        layout(base, L);
+        c0_load<NX>(a.ops[k], L);
+        C0Cycle<NX / 2>::load(base + 13 * FullG<NX>::S, a, k + 1);
+    }
+    __device__ __noinline__ static void run(double* base, const double* lu, const int* perm, int pre,
+                                            int post)
+    {
+        constexpr int NC = NX / 2;
+        constexpr int PB = 8 + 4 * (3 - DEPTH); // probe slots: level 31 -> 8.., 15 -> 12.., 7 -> 16..
+        C0Level<NX> L;
+        layout(base, L);
+        double* cbase = base + 13 * FullG<NX>::S;
+        C0Level<NC> Lc;
+        C0Cycle<NC>::layout(cbase, Lc);
+        for (int s = 0; s < pre; ++s) c0_sweep<true, NX>(L);
+        probe(0, PB);
+        c0_residual<NX>(L);
+        for (int I = threadIdx.x; I < NC * NC; I += blockDim.x) {
+            const int cy = I / NC, cx = I - cy * NC;
+            const int ci = FullG<NC>::xi(cx, cy);
+            Lc.b[ci] = restrict_from([&](int gx, int gy) { return L.r[FullG<NX>::xi(gx, gy)]; }, cx, cy);
+            Lc.x[ci] = 0.0;
+        }
+        __syncthreads();
+        probe(0, PB + 1);
+        C0Cycle<NC>::run(cbase, lu, perm, pre, post);
+        probe(0, PB + 2);
+        for (int i = threadIdx.x; i < NX * NX; i += blockDim.x) {
+            const int gy = i / NX, gx = i - gy * NX;
+            const int me = FullG<NX>::xi(gx, gy);
+            L.x[me] += prolong_from<NC>([&](int u, int v) { return Lc.x[FullG<NC>::xi(u, v)]; }, gx, gy);
+        }
+        __syncthreads();
+        for (int s = 0; s < post; ++s) c0_sweep<false, NX>(L);
+        probe(0, PB + 3);
+    }
+};
+
+template <>
+struct C0Cycle<3> { // level 2: dense 9x9 LU solve (DenseFactor::solve), factor in shared memory
+    static constexpr int DEPTH = 0;
+    static constexpr size_t doubles() { return 13 * (size_t)FullG<3>::S; }
+    __device__ static void layout(double* base, C0Level<3>& L)
+    {
+        constexpr int S = FullG<3>::S;
+        L.coef = base;
+        L.x = base + 9 * S;
+        L.b = L.x + S;
+        L.inv = L.b + S;
+        L.r = L.inv + S;
+    }
+    __device__ static void load(double*, const BottomArgs&, int) {}
+    __device__ static void run(double* base, const double* lu, const int* perm, int, int)
+    {
+        C0Level<3> L;
+        layout(base, L);
+        if (threadIdx.x == 0) {
+            double y[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const int q = perm[i];
+                y[i] = L.b[FullG<3>::xi(q % 3, q / 3)];
+            }
+#pragma unroll
+            for (int i = 0; i < 9; ++i)
+#pragma unroll
+                for (int k2 = 0; k2 < i; ++k2) y[i] -= lu[k2 * 9 + i] * y[k2];
+#pragma unroll
+            for (int i = 8; i >= 0; --i) {
+#pragma unroll
+                for (int k2 = i + 1; k2 < 9; ++k2) y[i] -= lu[k2 * 9 + i] * y[k2];
+                y[i] /= lu[i * 9 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 9; ++i) L.x[FullG<3>::xi(i % 3, i / 3)] = y[i];
+        }
+        __syncthreads();
+    }
+};
+
+// ----------------------------------------------------------- shared layout
+template <int TOP>
+struct Lay {
+    using G0 = SlabG<(1 << TOP) - 1, TOP == 7 ? 8 : 4>; // top slab level
+    using G1 = SlabG<63, 4>;                             // level 6 below a level-7 top
+    static constexpr bool S1 = TOP == 7;
+    static constexpr int BARS = 0; // 8 mbarriers (4 per slab level)
+    static constexpr int X0 = BARS + 8;
+    static constexpr int R0 = X0 + G0::XS;
+    static constexpr int X1 = R0 + G0::RS;
+    static constexpr int R1 = X1 + (S1 ? G1::XS : 0);
+    static constexpr int C1 = R1 + (S1 ? G1::RS : 0); // coef [4 colours][9][GROUP1]
+    static constexpr int I1 = C1 + (S1 ? 36 * G1::GROUP : 0);
+    static constexpr int B1 = I1 + (S1 ? 4 * G1::GROUP : 0);
+    static constexpr int RED = B1 + (S1 ? 4 * G1::GROUP : 0); // cluster reduction slots
+    static constexpr int LU = RED + kCS;                      // 81 LU + 9 perm (as int)
+    static constexpr int C0BASE = LU + 96;                    // CTA-0 levels (31, 15, 7, 3)
+    static constexpr size_t total() { return (size_t)C0BASE + C0Cycle<31>::doubles(); }
+};
+
 template <int TOP>
 __global__ void __launch_bounds__(kCT, 1)
     k_bottom_cluster(BottomArgs a, const double* __restrict__ bg, double* __restrict__ xg,
                      int cycles, int pre, int post, int check, double* state, int* flags)
 {
-    using G = Geo<TOP>;
-    constexpr int NX0 = G::nx(0), RP0 = G::rp(0);
-    constexpr int NX1 = G::nx(1), RP1 = G::rp(1);
-    constexpr bool S1 = G::slab(1); // TOP = 7: levels 7 and 6 are slab levels
-    constexpr int OFF1 = G::woff(1);
-    constexpr int C0 = G::first_c0();
-    extern __shared__ double smem[];
-    __shared__ double red[64];
+    using Ly = Lay<TOP>;
+    using G0 = typename Ly::G0;
+    using G1 = typename Ly::G1;
+    constexpr int NX0 = G0::NX, RP0 = G0::RP;
+    constexpr int NC = 31; // first CTA-0 level
+    extern __shared__ double sm[];
+    __shared__ double red[33];
     cg::cluster_group cl = cg::this_cluster();
-    const unsigned rank = cl.block_rank();
-    probe(rank, 0);
+    const int w = (int)cl.block_rank();
+    probe(w, 0);
 
-    Slab<NX0, RP0> s0(smem + G::woff(0), rank);
-    Slab<NX1, RP1> s1(smem + OFF1, rank); // only meaningful when S1
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Ly::BARS);
+    double* x0 = sm + Ly::X0;
+    double* r0s = sm + Ly::R0;
+    double* x1 = sm + Ly::X1;
+    double* r1s = sm + Ly::R1;
+    double* c1 = sm + Ly::C1;
+    double* i1 = sm + Ly::I1;
+    double* b1 = sm + Ly::B1;
+    double* lus = sm + Ly::LU;
+    int* perms = reinterpret_cast<int*>(lus + 81);
+    double* c0base = sm + Ly::C0BASE;
+    C0Level<NC> L5;
+    C0Cycle<NC>::layout(c0base, L5);
 
-    // ---- load operators and the top-level rhs
-    if (rank != 0) {
-        load_op(a.ops[0], NX0, s0.r0, s0.r1, Slab<NX0, RP0>::CNT, s0.coef, s0.inv);
-        for (int idx = threadIdx.x; idx < (s0.r1 - s0.r0) * NX0; idx += blockDim.x) {
-            s0.x[idx] = 0.0;
-            s0.b[idx] = bg[(long long)s0.r0 * NX0 + idx];
+    const Own<G0> o0(w);
+    const Own<G1> o1(w);
+    Halo<G0> H0;
+    H0.setup(bars, x0, w);
+    Halo<G1> H1;
+    H1.setup(bars + 4, x1, w);
+    if (threadIdx.x == 0) {
+        H0.init_barriers();
+        if constexpr (Ly::S1) H1.init_barriers();
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+
+    // ---- load: the top level's four rows per thread into registers, the rest into shared memory
+    double ra[4][9], rinv[4], rb[4];
+    {
+        const Op9& A = a.ops[0];
+        const long long n = (long long)NX0 * NX0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (o0.valid(c)) {
+                const long long gi = (long long)o0.gy(c) * NX0 + o0.gx(c);
+#pragma unroll
+                for (int d = 0; d < 9; ++d) ra[c][d] = op_entry(A, d, n, gi);
+                rinv[c] = 1.0 / ra[c][4];
+                rb[c] = bg[gi];
+            } else {
+#pragma unroll
+                for (int d = 0; d < 9; ++d) ra[c][d] = 0.0;
+                rinv[c] = rb[c] = 0.0;
+            }
         }
-        for (int i = threadIdx.x; i < 2 * NX0; i += blockDim.x) s0.ha[i] = 0.0; // ha, hb contiguous
-        if constexpr (S1)
-            load_op(a.ops[1], NX1, s1.r0, s1.r1, Slab<NX1, RP1>::CNT, s1.coef, s1.inv);
-    } else {
-        for (int k = C0; k < G::NLEV; ++k) {
-            const int nx = (1 << (TOP - k)) - 1;
-            double* base = smem + G::coff(k);
-            load_op(a.ops[k], nx, 0, nx, nx * nx, base, base + 11 * nx * nx);
+        for (int i = threadIdx.x; i < G0::XS; i += blockDim.x) x0[i] = 0.0;
+    }
+    if constexpr (Ly::S1) {
+        const Op9& A = a.ops[1];
+        const long long n = (long long)G1::NX * G1::NX;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (o1.valid(c)) {
+                const long long gi = (long long)o1.gy(c) * G1::NX + o1.gx(c);
+#pragma unroll
+                for (int d = 0; d < 9; ++d) {
+                    const double v = op_entry(A, d, n, gi);
+                    c1[(c * 9 + d) * G1::GROUP + threadIdx.x] = v;
+                    if (d == 4) i1[o1.slot(c)] = 1.0 / v;
+                }
+            }
         }
+    }
+    if (w == 0) {
+        C0Cycle<NC>::load(c0base, a, Ly::S1 ? 2 : 1);
+        if (threadIdx.x < 81) lus[threadIdx.x] = a.lu[threadIdx.x];
+        if (threadIdx.x < 9) perms[threadIdx.x] = a.perm[threadIdx.x];
     }
     cl.sync();
-    probe(rank, 1);
+    probe(w, 1);
 
-    auto top_norm = [&](const double* v) -> double {
-        double acc = 0.0;
-        if (rank != 0)
-            for (int idx = threadIdx.x; idx < (s0.r1 - s0.r0) * NX0; idx += blockDim.x)
-                acc += v[idx] * v[idx];
-        acc = block_sum(acc, red);
-        if (threadIdx.x == 0) {
-            double* dst = cl.map_shared_rank(&red[34], 0);
-            dst[rank] = acc;
+    // GS update of the thread's colour-c top-level node (register rows)
+    auto upd0 = [&](int c) -> double {
+        double s = rb[c];
+#pragma unroll
+        for (int d = 0; d < 9; ++d) {
+            if (d == 4) continue;
+            s -= ra[c][d] * xnb(x0, o0, c, d % 3 - 1, d / 3 - 1);
         }
+        return s * rinv[c];
+    };
+    auto upd1 = [&](int c) -> double {
+        double s = b1[o1.slot(c)];
+#pragma unroll
+        for (int d = 0; d < 9; ++d) {
+            if (d == 4) continue;
+            s -= c1[(c * 9 + d) * G1::GROUP + threadIdx.x] * xnb(x1, o1, c, d % 3 - 1, d / 3 - 1);
+        }
+        return s * i1[o1.slot(c)];
+    };
+    // cluster-wide sum of per-thread values; the result is valid in CTA 0 thread 0
+    auto cluster_sum = [&](double v) -> double {
+        v = block_sum(v, red);
+        if (threadIdx.x == 0) cl.map_shared_rank(sm + Ly::RED, 0)[w] = v;
         cl.sync();
         double tot = 0.0;
-        if (rank == 0 && threadIdx.x == 0)
-            for (int q = 0; q < kCS; ++q) tot += red[34 + q];
+        if (w == 0 && threadIdx.x == 0)
+            for (int q = 0; q < kCS; ++q) tot += sm[Ly::RED + q];
         cl.sync();
-        return sqrt(tot);
+        return tot;
     };
+    // residual of the top level at the thread's nodes (stored for the restriction); returns sum r^2
+    auto top_residual = [&]() -> double {
+        H0.ensure_all();
+        double r2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (o0.valid(c)) {
+                double s = 0.0;
+#pragma unroll
+                for (int d = 0; d < 9; ++d) s += ra[c][d] * xnb(x0, o0, c, d % 3 - 1, d / 3 - 1);
+                const double r = rb[c] - s;
+                r0s[(o0.gy(c) - RP0 * w) * NX0 + o0.gx(c)] = r;
+                r2 += r * r;
+            }
+        }
+        return r2;
+    };
+    // prolongate a coarse correction into a slab level: own nodes, then the two
+    // halo rows recomputed from the same parents (the neighbour does the same)
+    auto prolong_slab = [&](auto geo, double* xs, const auto& own, const auto& cxv) {
+        using GG = decltype(geo);
+        constexpr int NXF = GG::NX, RPF = GG::RP, NXC = NXF / 2;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (own.valid(c)) xs[own.me(c)] += prolong_from<NXC>(cxv, own.gx(c), own.gy(c));
+        const int t = threadIdx.x;
+        if (t < 2 * NXF) {
+            const int gx = t % NXF, side = t / NXF;
+            const int lr = side ? RPF + 1 : 0;
+            const int gy = RPF * w + lr - 1;
+            if (gy >= 0 && gy < NXF) xs[GG::xi(gx, lr)] += prolong_from<NXC>(cxv, gx, gy);
+        }
+        cl.sync(); // neighbours finish reading their old halo values before new pushes
+    };
+
     double prev = 0.0;
-    if (check) prev = top_norm(s0.b);
+    if (check) {
+        double b2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) b2 += rb[c] * rb[c];
+        prev = sqrt(cluster_sum(b2));
+    }
 
     for (int cyc = 0; cyc < cycles; ++cyc) {
-        // ===================== level 0 (slab) down
-        for (int s = 0; s < pre; ++s) slab_sweep<NX0, RP0>(cl, s0, true, G::woff(0), smem);
-        probe(rank, 2);
-        slab_residual<NX0, RP0>(s0);
+        // ===================== top slab level: pre-smoothing, residual
+        for (int s = 0; s < pre; ++s) slab_sweep<true>(x0, H0, o0, upd0);
+        top_residual();
         cl.sync();
-        probe(rank, 3);
-        if constexpr (S1) {
-            // restrict into the level-1 slab rows this CTA owns (fine rows may be remote)
-            if (rank != 0) {
-                auto fr = [&](int gx, int gy) -> double {
-                    const int owner = gy / RP0 + 1;
-                    const double* rr = (owner == (int)rank)
-                                           ? s0.r
-                                           : cl.map_shared_rank(s0.r, (unsigned)owner);
-                    return rr[(gy - (owner - 1) * RP0) * NX0 + gx];
-                };
-                for (int idx = threadIdx.x; idx < (s1.r1 - s1.r0) * NX1; idx += blockDim.x) {
-                    const int ly = idx / NX1, cx = idx - ly * NX1;
-                    s1.b[idx] = restrict_from(fr, cx, s1.r0 + ly);
-                    s1.x[idx] = 0.0;
-                }
-                for (int i = threadIdx.x; i < 2 * NX1; i += blockDim.x) s1.ha[i] = 0.0;
-            }
-            cl.sync();
-            probe(rank, 4);
-            // ===================== level 1 (slab) down
-            for (int s = 0; s < pre; ++s) slab_sweep<NX1, RP1>(cl, s1, true, OFF1, smem);
-            probe(rank, 5);
-            slab_residual<NX1, RP1>(s1);
-            cl.sync();
-            probe(rank, 6);
-        }
-        // restrict the last slab level into CTA 0's first coarse level
-        constexpr int NLS = S1 ? NX1 : NX0; // last slab level size
-        constexpr int RPLS = S1 ? RP1 : RP0;
-        constexpr int NC = G::nx(C0);
-        if (rank == 0) {
-            const double* rloc = S1 ? s1.r : s0.r;
-            double* cb = smem + G::coff(C0) + 10 * NC * NC;
-            double* cxv = smem + G::coff(C0) + 9 * NC * NC;
-            auto fr = [&](int gx, int gy) -> double {
-                const int owner = gy / RPLS + 1;
-                const double* rr = cl.map_shared_rank(rloc, (unsigned)owner);
-                return rr[(gy - (owner - 1) * RPLS) * NLS + gx];
+        probe(w, 2);
+        if constexpr (Ly::S1) {
+            // restrict into this CTA's level-6 rows (fine row 2J+2 may be remote)
+            auto fr0 = [&](int gx, int gy) -> double {
+                const int owner = gy / RP0;
+                const double* rr = owner == w ? r0s : cl.map_shared_rank(r0s, (unsigned)owner);
+                return rr[(gy - owner * RP0) * NX0 + gx];
             };
-            for (int I = threadIdx.x; I < NC * NC; I += blockDim.x) {
-                const int cy = I / NC, cxx = I - cy * NC;
-                cb[I] = restrict_from(fr, cxx, cy);
-                cxv[I] = 0.0;
-            }
-            __syncthreads();
-            probe(rank, 7);
-            // ===================== CTA-0 levels (<= 31 per side) and the LU solve
-            if (threadIdx.x < G::c0threads(C0)) C0Down<TOP, C0>::run(smem, a, pre, post);
-            probe(rank, 8);
-        }
-        cl.sync();
-        probe(rank, 9);
-        // ===================== prolongate CTA 0's correction into the last slab level
-        {
-            const double* c0x = cl.map_shared_rank(smem + G::coff(C0) + 9 * NC * NC, 0);
-            auto cxv = [&](int u, int v) { return c0x[v * NC + u]; };
-            if constexpr (S1) {
-                if (rank != 0)
-                    for (int idx = threadIdx.x; idx < (s1.r1 - s1.r0) * NX1; idx += blockDim.x) {
-                        const int ly = idx / NX1, gx = idx - ly * NX1, gy = s1.r0 + ly;
-                        const double v = s1.x[idx] + prolong_from<NC>(cxv, gx, gy);
-                        s1.x[idx] = v;
-                        push_halo(cl, s1, gx, gy, v, OFF1, smem);
-                    }
-                cl.sync();
-                probe(rank, 10);
-                for (int s = 0; s < post; ++s) slab_sweep<NX1, RP1>(cl, s1, false, OFF1, smem);
-                probe(rank, 11);
-                // prolongate level 1 into level 0 (coarse rows may be remote)
-                if (rank != 0) {
-                    auto c1x = [&](int u, int v) -> double {
-                        const int owner = v / RP1 + 1;
-                        const double* xx = (owner == (int)rank)
-                                               ? s1.x
-                                               : cl.map_shared_rank(s1.x, (unsigned)owner);
-                        return xx[(v - (owner - 1) * RP1) * NX1 + u];
-                    };
-                    for (int idx = threadIdx.x; idx < (s0.r1 - s0.r0) * NX0; idx += blockDim.x) {
-                        const int ly = idx / NX0, gx = idx - ly * NX0, gy = s0.r0 + ly;
-                        const double v = s0.x[idx] + prolong_from<NX1>(c1x, gx, gy);
-                        s0.x[idx] = v;
-                        push_halo(cl, s0, gx, gy, v, G::woff(0), smem);
-                    }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (o1.valid(c)) b1[o1.slot(c)] = restrict_from(fr0, o1.gx(c), o1.gy(c));
+            for (int i = threadIdx.x; i < G1::XS; i += blockDim.x) x1[i] = 0.0;
+            cl.sync();
+            for (int s = 0; s < pre; ++s) slab_sweep<true>(x1, H1, o1, upd1);
+            H1.ensure_all();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (o1.valid(c)) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int d = 0; d < 9; ++d)
+                        sum += c1[(c * 9 + d) * G1::GROUP + threadIdx.x] * xnb(x1, o1, c, d % 3 - 1, d / 3 - 1);
+                    r1s[(o1.gy(c) - G1::RP * w) * G1::NX + o1.gx(c)] = b1[o1.slot(c)] - sum;
                 }
-            } else {
-                if (rank != 0)
-                    for (int idx = threadIdx.x; idx < (s0.r1 - s0.r0) * NX0; idx += blockDim.x) {
-                        const int ly = idx / NX0, gx = idx - ly * NX0, gy = s0.r0 + ly;
-                        const double v = s0.x[idx] + prolong_from<NC>(cxv, gx, gy);
-                        s0.x[idx] = v;
-                        push_halo(cl, s0, gx, gy, v, G::woff(0), smem);
-                    }
             }
             cl.sync();
-            probe(rank, 12);
+            probe(w, 3);
         }
-        for (int s = 0; s < post; ++s) slab_sweep<NX0, RP0>(cl, s0, false, G::woff(0), smem);
-        probe(rank, 13);
+        // restrict the last slab level into CTA 0's level-5 b (distributed, DSM stores)
+        {
+            using GS = std::conditional_t<Ly::S1, G1, G0>;
+            const double* rl = Ly::S1 ? r1s : r0s;
+            auto frs = [&](int gx, int gy) -> double {
+                const int owner = gy / GS::RP;
+                const double* rr = owner == w ? rl : cl.map_shared_rank(rl, (unsigned)owner);
+                return rr[(gy - owner * GS::RP) * GS::NX + gx];
+            };
+            double* b5 = cl.map_shared_rank(L5.b, 0);
+            double* x5 = cl.map_shared_rank(L5.x, 0);
+            // coarse rows J whose centre fine row 2J+1 lies in this CTA's band
+            const int J0 = (GS::RP * w) / 2, J1 = min((GS::RP * w + GS::RP) / 2, NC);
+            for (int i = threadIdx.x; i < (J1 - J0) * NC; i += blockDim.x) {
+                const int J = J0 + i / NC, I = i - (i / NC) * NC;
+                const int ci = FullG<NC>::xi(I, J);
+                b5[ci] = restrict_from(frs, I, J);
+                x5[ci] = 0.0;
+            }
+        }
+        cl.sync();
+        probe(w, 4);
+        // ===================== CTA-0 levels and the LU solve
+        if (w == 0) C0Cycle<NC>::run(c0base, lus, perms, pre, post);
+        cl.sync();
+        probe(w, 5);
+        // ===================== prolongations and post-smoothing
+        {
+            const double* c5x = cl.map_shared_rank(L5.x, 0);
+            auto cx5 = [&](int u, int v) { return c5x[FullG<NC>::xi(u, v)]; };
+            if constexpr (Ly::S1) {
+                prolong_slab(G1{}, x1, o1, cx5);
+                for (int s = 0; s < post; ++s) slab_sweep<false>(x1, H1, o1, upd1);
+                H1.ensure_all();
+                // level-7 parents lie in this CTA's level-6 band or its halo rows
+                auto cx6 = [&](int u, int v) { return x1[G1::xi(u, v - G1::RP * w + 1)]; };
+                prolong_slab(G0{}, x0, o0, cx6);
+            } else {
+                prolong_slab(G0{}, x0, o0, cx5);
+            }
+        }
+        probe(w, 6);
+        for (int s = 0; s < post; ++s) slab_sweep<false>(x0, H0, o0, upd0);
+        probe(w, 7);
         if (check) {
-            slab_residual<NX0, RP0>(s0);
-            __syncthreads();
-            const double res = top_norm(s0.r);
-            if (rank == 0 && threadIdx.x == 0 && res > 10.0 * prev) atomicOr(flags, kErrMgDiverged);
+            const double res = sqrt(cluster_sum(top_residual()));
+            if (w == 0 && threadIdx.x == 0 && res > 10.0 * prev) atomicOr(flags, kErrMgDiverged);
             prev = res;
         }
+        H0.ensure_all();
     }
-    if (rank != 0)
-        for (int idx = threadIdx.x; idx < (s0.r1 - s0.r0) * NX0; idx += blockDim.x)
-            xg[(long long)s0.r0 * NX0 + idx] = s0.x[idx];
-    if (check && state && rank == 0 && threadIdx.x == 0) state[0] = prev;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        if (o0.valid(c)) xg[(long long)o0.gy(c) * NX0 + o0.gx(c)] = x0[o0.me(c)];
+    if (check && state && w == 0 && threadIdx.x == 0) state[0] = prev;
+    cl.sync(); // no CTA exits while a neighbour may still address its shared memory
+}
+
+template <int TOP>
+cudaLaunchConfig_t cluster_cfg(cudaStream_t s, cudaLaunchAttribute* at)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kCS);
+    cfg.blockDim = dim3(kCT);
+    cfg.dynamicSmemBytes = Lay<TOP>::total() * sizeof(double);
+    cfg.stream = s;
+    at->id = cudaLaunchAttributeClusterDimension;
+    at->val.clusterDim.x = kCS;
+    at->val.clusterDim.y = 1;
+    at->val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+template <int TOP>
+bool set_attrs()
+{
+    return cudaFuncSetAttribute(k_bottom_cluster<TOP>,
+                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+           cudaFuncSetAttribute(k_bottom_cluster<TOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(Lay<TOP>::total() * sizeof(double))) == cudaSuccess;
 }
 
 template <int TOP>
 void launch_top(cudaStream_t s, const BottomArgs& a, const double* b, double* x, int cycles,
                 int pre, int post, bool check, double* state, int* flags)
 {
-    const size_t smem = (size_t)Geo<TOP>::total() * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_bottom_cluster<TOP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(k_bottom_cluster<TOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr = true;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(kCS);
-    cfg.blockDim = dim3(kCT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
+    static const bool attr = set_attrs<TOP>();
+    (void)attr;
     cudaLaunchAttribute at{};
-    at.id = cudaLaunchAttributeClusterDimension;
-    at.val.clusterDim.x = kCS;
-    at.val.clusterDim.y = 1;
-    at.val.clusterDim.z = 1;
-    cfg.attrs = &at;
-    cfg.numAttrs = 1;
+    cudaLaunchConfig_t cfg = cluster_cfg<TOP>(s, &at);
     note_launch();
     cudaLaunchKernelEx(&cfg, k_bottom_cluster<TOP>, a, b, x, cycles, pre, post, check ? 1 : 0,
                        state, flags);
 }
 
-static_assert(Geo<7>::total() * 8 <= 220 * 1024, "level-7 cluster layout exceeds shared memory");
+static_assert(Lay<7>::total() * sizeof(double) <= 220 * 1024, "cluster layout exceeds shared memory");
 
 } // namespace
 
@@ -557,33 +815,19 @@ void cluster_probes(int enable, unsigned long long* out64)
 
 bool cluster_bottom_supported()
 {
-    static int supported = -1;
-    if (supported < 0) {
-        supported = 0;
-        const size_t smem = (size_t)Geo<7>::total() * sizeof(double);
-        if (cudaFuncSetAttribute(k_bottom_cluster<7>,
-                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
-            cudaFuncSetAttribute(k_bottom_cluster<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) == cudaSuccess) {
-            cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(kCS);
-            cfg.blockDim = dim3(kCT);
-            cfg.dynamicSmemBytes = smem;
+    static const bool supported = [] {
+        bool ok = set_attrs<7>() && set_attrs<6>();
+        if (ok) {
             cudaLaunchAttribute at{};
-            at.id = cudaLaunchAttributeClusterDimension;
-            at.val.clusterDim.x = kCS;
-            at.val.clusterDim.y = 1;
-            at.val.clusterDim.z = 1;
-            cfg.attrs = &at;
-            cfg.numAttrs = 1;
+            cudaLaunchConfig_t cfg = cluster_cfg<7>(nullptr, &at);
             int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, k_bottom_cluster<7>, &cfg) == cudaSuccess &&
-                nclusters > 0)
-                supported = 1;
+            ok = cudaOccupancyMaxActiveClusters(&nclusters, k_bottom_cluster<7>, &cfg) == cudaSuccess &&
+                 nclusters > 0;
         }
         cudaGetLastError();
-    }
-    return supported == 1;
+        return ok;
+    }();
+    return supported;
 }
 
 void launch_bottom_cluster(cudaStream_t s, const ClusterArgs& a, const double* b, double* x,
