@@ -37,8 +37,10 @@ typedef struct oc_mg oc_mg;           /* standalone multigrid hierarchy */
 enum { OC_PDE_POISSON = 0, OC_PDE_CONVDIFF = 1, OC_PDE_HEAT = 2 };
 /* SolverKind (ipm.hpp:15); OC_SOLVER_DENSE is not offered on the device */
 enum { OC_SOLVER_GMRES_PT = 0, OC_SOLVER_MINRES_PD = 1, OC_SOLVER_GMRES_PPI = 2 };
-/* smoother: 4-colour symmetric Gauss-Seidel (default) */
-enum { OC_SMOOTHER_COLOR4 = 0 };
+/* smoother: 4-colour symmetric Gauss-Seidel (default, parallel), or the
+ * reference's lexicographic Gauss-Seidel (multigrid.cpp:44-66) run as a
+ * skewed wavefront (faithful mode) */
+enum { OC_SMOOTHER_COLOR4 = 0, OC_SMOOTHER_LEX = 1 };
 /* preconditioner kinds for oc_precond_apply */
 enum { OC_PRECOND_PD = 0, OC_PRECOND_PT = 1, OC_PRECOND_PPI = 2 };
 
@@ -167,9 +169,9 @@ int oc_time_applies(oc_problem* prob, int kind, int reps, double* kkt_ms, double
 /* MgHierarchy over an explicit 9-point operator (multigrid.hpp:43-64):
  * coef9 = 9 arrays of n values (SW,S,SE,W,C,E,NW,N,NE), host or device.
  * rediscretize: 0 plain Galerkin, 1 convdiff(eps) base per level,
- * 2 transposed convdiff base. */
+ * 2 transposed convdiff base. smoother: OC_SMOOTHER_*. */
 int oc_mg_create(oc_ctx* ctx, int level, const double* coef9, int rediscretize, double eps,
-                 oc_mg** out);
+                 int smoother, oc_mg** out);
 int oc_mg_solve(oc_mg* mg, const double* rhs, int cycles, int pre, int post, double* out);
 int oc_mg_depth(oc_mg* mg);
 int oc_mg_level_matrix(oc_mg* mg, int k, double* coef9);

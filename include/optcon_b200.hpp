@@ -72,6 +72,9 @@ struct IpmParams {
     int linear_maxit = 200, cheb_steps = 20, mg_cycles = 3, mg_pre = 5, mg_post = 5;
     SolverKind solver = SolverKind::gmres_pt;
     int gmres_restart = 0;
+    /// OC_SMOOTHER_COLOR4 (parallel default) or OC_SMOOTHER_LEX (the
+    /// reference's lexicographic Gauss-Seidel, faithful mode)
+    int smoother = OC_SMOOTHER_COLOR4;
 
     oc_ipm_params c() const
     {
@@ -80,7 +83,7 @@ struct IpmParams {
         p.mu0 = mu0; p.max_iterations = max_iterations; p.linear_tol = linear_tol;
         p.linear_maxit = linear_maxit; p.cheb_steps = cheb_steps; p.mg_cycles = mg_cycles;
         p.mg_pre = mg_pre; p.mg_post = mg_post; p.solver = static_cast<int>(solver);
-        p.smoother = OC_SMOOTHER_COLOR4; p.gmres_restart = gmres_restart;
+        p.smoother = smoother; p.gmres_restart = gmres_restart;
         return p;
     }
 };

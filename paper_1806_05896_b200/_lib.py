@@ -136,7 +136,7 @@ def load():
     L.oc_ipm_pieces.argtypes = [vp] * 8 + [C.c_double, C.c_double] + [vp] * 7
     L.oc_objective.argtypes = [vp, vp, vp, _dp]
     L.oc_time_applies.argtypes = [vp, C.c_int, C.c_int, _dp, _dp]
-    L.oc_mg_create.argtypes = [vp, C.c_int, vp, C.c_int, C.c_double, C.POINTER(C.c_void_p)]
+    L.oc_mg_create.argtypes = [vp, C.c_int, vp, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_void_p)]
     L.oc_mg_solve.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp]
     L.oc_mg_level_matrix.argtypes = [vp, C.c_int, vp]
     L.oc_mg_smooth.argtypes = [vp, vp, vp, C.c_int]

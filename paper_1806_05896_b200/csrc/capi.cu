@@ -261,7 +261,7 @@ int oc_time_applies(oc_problem* p, int kind, int reps, double* kkt_ms, double* p
 }
 
 int oc_mg_create(oc_ctx* c, int level, const double* coef9, int rediscretize, double eps,
-                 oc_mg** out)
+                 int smoother, oc_mg** out)
 {
     return guarded([&] {
         require(c, "oc_mg_create");
@@ -274,7 +274,7 @@ int oc_mg_create(oc_ctx* c, int level, const double* coef9, int rediscretize, do
         const long long n = ocb::level_n(level);
         m->fine.resize(9 * (size_t)n);
         ocb::copy_any(c->ctx, m->fine.get(), coef9, 9 * (size_t)n * 8);
-        m->h.allocate(level);
+        m->h.allocate(level, 1, smoother);
         ocb::Op9 f{};
         f.nx = ocb::level_nx(level);
         f.coef = m->fine.get();
@@ -319,6 +319,8 @@ int oc_mg_solve(oc_mg* m, const double* rhs, int cycles, int pre, int post, doub
         m->ctx->sync();
         if (m->ctx->hflags[0] & ocb::kErrMgDiverged)
             throw ocb::RuntimeError("MgHierarchy::solve: residual growth, cycle diverged");
+        if (m->ctx->hflags[0] & ocb::kErrLexStall)
+            throw ocb::RuntimeError("gauss_seidel_sweep: wavefront hand-off stalled");
     });
 }
 

@@ -13,6 +13,7 @@
 // lexicographic sweep: it keeps the V-cycle SPD for
 // symmetric operators, which MINRES with P_D requires.
 #include "kernels.hpp"
+#include "lex_gs.cuh"
 
 #include <algorithm>
 #include <stdexcept>
@@ -379,6 +380,66 @@ __device__ void bt_sweep(const Op9& A, const double* bsm, double* xsm, bool forw
     }
 }
 
+// Lexicographic sweep of one bottom level in shared memory (lex_gs.cuh): warps
+// 0..ceil(nx/32)-1 run the skewed wavefront; the hand-off between them goes
+// through the shared mailbox mbs (sentinel-filled, restored on return).
+__device__ void bt_sweep_lex(const Op9& A, const double* bsm, double* xsm, volatile double* mbs,
+                             bool fwd)
+{
+    const int nx = A.nx;
+    const long long n = (long long)nx * nx;
+    const int wid = threadIdx.x >> 5, j = threadIdx.x & 31;
+    const int nw = (nx + 31) >> 5;
+    if (wid < nw) {
+        const int r = 32 * wid + j;
+        const bool rowok = r < nx, hasN = r + 1 < nx;
+        const int sx = fwd ? 1 : -1, sy = fwd ? nx : -nx;
+        const int row0 = fwd ? r * nx : (nx - 1 - r) * nx + (nx - 1);
+        const bool consumer = j == 0 && wid > 0, producer = j == 31 && hasN;
+        volatile double* mb_in = mbs + (wid > 0 ? wid - 1 : 0) * nx;
+        volatile double* mb_out = mbs + wid * nx;
+        double sw = 0.0, s = 0.0, se = 0.0, last = 0.0, n_prev = 0.0;
+        for (int st = -1; st < nx + 62; ++st) {
+            const int xl = st - 2 * j;
+            double up = __shfl_up_sync(0xffffffffu, last, 1);
+            if (j == 0) {
+                up = 0.0;
+                const int xe = st + 1;
+                if (consumer && xe < nx) {
+                    double v = mb_in[xe];
+                    while (lex_is_sentinel(v)) v = mb_in[xe];
+                    up = v;
+                    mb_in[xe] = lex_sentinel();
+                }
+            }
+            sw = s;
+            s = se;
+            se = up;
+            double v = 0.0, nn = 0.0;
+            if (rowok && xl >= 0 && xl < nx) {
+                const int i = row0 + xl * sx;
+                const bool hasE = xl + 1 < nx;
+                const double e = hasE ? xsm[i + sx] : 0.0;
+                double ne = 0.0;
+                if (hasN) {
+                    nn = xsm[i + sy];
+                    if (hasE) ne = xsm[i + sy + sx];
+                }
+                auto a = [&](int d) -> double {
+                    const int dp = fwd ? d : 8 - d;
+                    return A.coef ? A.coef[dp * n + i] : A.c[dp];
+                };
+                v = lex_update(a, bsm[i], 1.0 / diag_at(A, i, n), sw, s, se, last, e, n_prev, nn, ne);
+                xsm[i] = v;
+                if (producer) mb_out[xl] = v;
+            }
+            n_prev = nn;
+            last = v;
+        }
+    }
+    __syncthreads();
+}
+
 __device__ double bt_resid_sq(const Op9& A, const double* bsm, const double* xsm, double* red)
 {
     const int nx = A.nx;
@@ -413,6 +474,8 @@ __global__ void __launch_bounds__(kBottomThreads) k_bottom(BottomArgs a, const d
     }
     double* rs = p;
     const int n0 = a.ops[0].nx * a.ops[0].nx;
+    volatile double* mbs = rs + n0; // lexicographic hand-off mailbox (64 slots)
+    if (a.lex && threadIdx.x < 64) mbs[threadIdx.x] = lex_sentinel();
     for (int i = threadIdx.x; i < n0; i += blockDim.x) {
         bs[0][i] = bg[i];
         xs[0][i] = 0.0;
@@ -433,7 +496,10 @@ __global__ void __launch_bounds__(kBottomThreads) k_bottom(BottomArgs a, const d
     for (int cyc = 0; cyc < cycles; ++cyc) {
         for (int k = 0; k < last; ++k) {
             const Op9& A = a.ops[k];
-            for (int s = 0; s < pre; ++s) bt_sweep(A, bs[k], xs[k], true);
+            for (int s = 0; s < pre; ++s) {
+                if (a.lex) bt_sweep_lex(A, bs[k], xs[k], mbs, true);
+                else bt_sweep(A, bs[k], xs[k], true);
+            }
             const int nx = A.nx, nxc = (nx - 1) / 2;
             for (int i = threadIdx.x; i < nx * nx; i += blockDim.x)
                 rs[i] = bs[k][i] - op_apply_at(A, xs[k], i % nx, i / nx);
@@ -472,7 +538,10 @@ __global__ void __launch_bounds__(kBottomThreads) k_bottom(BottomArgs a, const d
             for (int i = threadIdx.x; i < nx * nx; i += blockDim.x)
                 xs[k][i] = xs[k][i] + prolong_at(xs[k + 1], nxc, i % nx, i / nx);
             __syncthreads();
-            for (int s = 0; s < post; ++s) bt_sweep(A, bs[k], xs[k], false);
+            for (int s = 0; s < post; ++s) {
+                if (a.lex) bt_sweep_lex(A, bs[k], xs[k], mbs, false);
+                else bt_sweep(A, bs[k], xs[k], false);
+            }
         }
         if (check) {
             const double res = sqrt(bt_resid_sq(a.ops[0], bs[0], xs[0], red));
@@ -568,6 +637,7 @@ size_t bottom_smem_bytes(const BottomArgs& a)
     size_t m = 0;
     for (int k = 0; k < a.nlev; ++k) m += 2ull * a.ops[k].nx * a.ops[k].nx;
     m += (size_t)a.ops[0].nx * a.ops[0].nx;
+    m += 64; // lexicographic hand-off mailbox
     return m * sizeof(double);
 }
 

@@ -22,6 +22,7 @@ constexpr int kBottomTopLevel = 6;    // grid levels <= this run inside one CTA
 
 struct BottomArgs {
     int nlev;                          // number of levels handled (top .. level 2)
+    int lex;                           // lexicographic (reference) smoother instead of 4-colour
     Op9 ops[kBottomMaxLevels];         // [0] = top level of the bottom solver
     const double* lu;                  // 9x9 LU of the level-2 matrix (column-major)
     const int* perm;
@@ -74,6 +75,13 @@ void launch_coarse_lu(cudaStream_t s, const double* coef9, double* lu, int* perm
 // whole V-cycle below (and including) the bottom top level in one CTA
 void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double* x, int cycles,
                    int pre, int post, bool check, double* state, int* flags);
+
+// k_mg_lex.cu: one lexicographic Gauss-Seidel sweep in place (the reference
+// smoother, multigrid.cpp:44-66) as a skewed wavefront; inv = 1/diag(A);
+// mbox = ceil(nx/32) * nx doubles holding kLexSentinel (restored on return).
+void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* inv, double* x,
+                   bool forward, double* mbox, int* flags);
+double lex_sentinel_host();
 
 // Cluster-resident bottom (k_mg_cluster.cu): levels <= 7 in one 16-CTA
 // thread-block cluster with distributed shared memory. ops[0] is the top

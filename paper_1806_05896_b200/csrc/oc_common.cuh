@@ -122,6 +122,7 @@ enum ErrFlag : int {
     kErrLamZb = 1 << 11,
     kErrThetaZ = 1 << 12,         // build_theta (ipm.cpp:44,56)
     kErrThetaY = 1 << 13,
+    kErrLexStall = 1 << 14,       // lexicographic wavefront hand-off never arrived
 };
 
 } // namespace ocb

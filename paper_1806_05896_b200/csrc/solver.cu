@@ -140,18 +140,24 @@ void copy_any(Ctx& c, void* dst, const void* src, size_t bytes)
 }
 
 // =================================================================== Hierarchy
-void Hierarchy::allocate(int level, int batch)
+void Hierarchy::allocate(int level, int batch, int smoother)
 {
     if (level < 3) throw InvalidArgument("MgHierarchy: fine level must be >= 3");
-    if (built_ && level == level_ && batch == batch_) return;
+    if (smoother != OC_SMOOTHER_COLOR4 && smoother != OC_SMOOTHER_LEX)
+        throw InvalidArgument("MgHierarchy: unknown smoother");
+    if (built_ && level == level_ && batch == batch_ && smoother == smoother_) return;
     level_ = level;
     batch_ = batch;
+    smoother_ = smoother;
+    lex_ = smoother == OC_SMOOTHER_LEX;
     K_ = level - 2;
     nx_.assign(K_ + 1, 0);
     for (int k = 0; k <= K_; ++k) nx_[k] = (1 << (level - k)) - 1;
     // levels <= 7 run in the 16-CTA cluster kernel when the top of that range
     // is a slab level (>= 6); otherwise levels <= 6 in the single-CTA kernel
-    cluster_ = level >= 6 && cluster_bottom_supported();
+    // (the cluster kernel smooths with 4 colours; the lexicographic mode keeps
+    // levels <= 6 in the single-CTA kernel and sweeps the others as wavefronts)
+    cluster_ = !lex_ && level >= 6 && cluster_bottom_supported();
     const int top = cluster_ ? kClusterTopLevel : kBottomTopLevel;
     kb_ = 0;
     while (level - kb_ > top) ++kb_;
@@ -174,6 +180,12 @@ void Hierarchy::allocate(int level, int batch)
     inv_.clear();
     inv_.resize(K_ + 1);
     for (int k = 0; k < kb_; ++k) inv_[k].resize((size_t)level_n(k) * batch);
+    if (lex_) {
+        const int nx0 = nx_[0];
+        mbox_.resize((size_t)((nx0 + 31) / 32) * nx0);
+    } else {
+        mbox_.release();
+    }
     lu_.resize(81 * (size_t)batch);
     perm_.resize(9 * (size_t)batch);
     part_.resize(kRedBlocks);
@@ -222,6 +234,7 @@ void Hierarchy::build_inv(Ctx& c)
         const long long ds = k == 0 ? fine_diag_stride_ : 0;
         launch_inv_diag(c.stream, a, inv_[k].get(), batch_, cs, ds);
     }
+    if (lex_) launch_fill(c.stream, mbox_.get(), lex_sentinel_host(), (long long)mbox_.size());
 }
 
 void Hierarchy::build_rediscretized(Ctx& c, const Op9& fine, const std::vector<const double*>& base)
@@ -256,6 +269,7 @@ BottomArgs Hierarchy::bottom_args(int kfrom, int bt) const
 {
     BottomArgs a{};
     a.nlev = K_ - kfrom + 1;
+    a.lex = lex_ ? 1 : 0;
     if (a.nlev > kBottomMaxLevels) throw RuntimeError("bottom solver: too many levels");
     for (int j = 0; j < a.nlev; ++j) a.ops[j] = level_op(kfrom + j, bt);
     a.lu = lu_.get() + 81 * (size_t)bt;
@@ -276,6 +290,18 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
         return;
     }
     const Op9 A = level_op(k, bt);
+    if (lex_) {
+        // reference cycle (multigrid.cpp:111-132) with in-place lexicographic sweeps
+        if (zero_in) launch_fill(c.stream, xout, 0.0, level_n(k));
+        for (int s = 0; s < p.pre; ++s)
+            launch_gs_lex(c.stream, A, b, inv_at(k, bt), xout, true, mbox_.get(), flags);
+        launch_resid_restrict_tiled(c.stream, A, b, xout, b_[k + 1].get(), xa_[k + 1].get());
+        vcycle(c, k + 1, b_[k + 1].get(), xa_[k + 1].get(), true, p, bt, flags);
+        launch_prolong_add(c.stream, nx_[k], xa_[k + 1].get(), xout);
+        for (int s = 0; s < p.post; ++s)
+            launch_gs_lex(c.stream, A, b, inv_at(k, bt), xout, false, mbox_.get(), flags);
+        return;
+    }
     double* Abuf = xout;
     double* Bbuf = xb_[k].get();
     // sweeps are fused g_sweep_fuse at a time (same colour-pass sequence)
@@ -361,6 +387,14 @@ void Hierarchy::smooth(Ctx& c, const double* b, double* x, bool forward, int bt)
     const Op9 A = level_op(0, bt);
     DVec inv((size_t)level_n(0));
     launch_inv_diag(c.stream, A, inv.get(), 1, 0, 0);
+    if (lex_) {
+        DevArray<int> fl(1);
+        cudaMemsetAsync(fl.get(), 0, sizeof(int), c.stream);
+        launch_gs_lex(c.stream, A, b, inv.get(), x, forward, mbox_.get(), fl.get());
+        c.sync();
+        launch_check("smoothing sweep");
+        return;
+    }
     launch_sweep_tiled(c.stream, A, b, inv.get(), x, xb_[0].get(), forward, false, nullptr, 1);
     launch_copy(c.stream, xb_[0].get(), x, level_n(0));
     c.sync();
@@ -648,6 +682,7 @@ void Problem::check_flags(bool sync_now)
     if (f & kErrSingular2x2) throw RuntimeError("block_2x2_inverse_apply: singular pivot block");
     if (f & kErrMgDiverged)
         throw RuntimeError("MgHierarchy::solve: residual growth, cycle diverged");
+    if (f & kErrLexStall) throw RuntimeError("gauss_seidel_sweep: wavefront hand-off stalled");
     if (f & kErrYInterior) throw RuntimeError("ipm: lost strict interiority in y");
     if (f & kErrLamYa) throw RuntimeError("ipm: multiplier not positive in lam_ya");
     if (f & kErrLamYb) throw RuntimeError("ipm: multiplier not positive in lam_yb");
@@ -686,21 +721,24 @@ void Problem::setup_precond(int kind, const oc_ipm_params& p)
     mg_.pre = p.mg_pre;
     mg_.post = p.mg_post;
     cheb_steps_ = p.cheb_steps;
+    if (p.smoother != OC_SMOOTHER_COLOR4 && p.smoother != OC_SMOOTHER_LEX)
+        throw InvalidArgument("ipm: unknown smoother");
+    smoother_ = p.smoother;
     int* fl = flags_.get();
     const double* ty = has_sb_ ? ty_.get() : nullptr;
     if (heat_) {
         // TimeSchurApprox (timedep.cpp:245-261): one hierarchy per time block on
         // M + tau L + diag(mhat_k), built as a batch
         launch_mhat(ctx.stream, P, nullptr, tw_.get(), tv_.get(), mhat_.get(), nullptr, fl);
-        Hheat_.allocate(level_, nt_);
+        Hheat_.allocate(level_, nt_, smoother_);
         Op9 f = P.Mtl;
         f.diag = mhat_.get();
         Hheat_.build(ctx, f, 0, ns_);
     } else if (kind == OC_PRECOND_PPI) {
         // PermutedPrecond (precond.cpp:262-285)
         launch_mhat(ctx.stream, P, nullptr, tw_.get(), tv_.get(), nullptr, bracket_.get(), fl);
-        if (!HL_built_) {
-            HL_.allocate(level_);
+        if (!HL_built_ || HL_.smoother() != smoother_) {
+            HL_.allocate(level_, 1, smoother_);
             if (convdiff_) {
                 std::vector<const double*> b;
                 for (auto& v : base_) b.push_back(v.get());
@@ -729,8 +767,8 @@ void Problem::setup_precond(int kind, const oc_ipm_params& p)
         left.diag = ty;
         Op9 right = P.L;
         right.diag = bracket_.get();
-        Hleft_.allocate(level_);
-        Hright_.allocate(level_);
+        Hleft_.allocate(level_, 1, smoother_);
+        Hright_.allocate(level_, 1, smoother_);
         if (convdiff_) {
             std::vector<const double*> b, bt;
             for (auto& v : base_) b.push_back(v.get());
@@ -746,7 +784,7 @@ void Problem::setup_precond(int kind, const oc_ipm_params& p)
         launch_mhat(ctx.stream, P, ty, tw_.get(), tv_.get(), mhat_.get(), nullptr, fl);
         Op9 F = P.L;
         F.diag = mhat_.get();
-        HF_.allocate(level_);
+        HF_.allocate(level_, 1, smoother_);
         if (convdiff_) {
             std::vector<const double*> b, bt;
             for (auto& v : base_) b.push_back(v.get());
@@ -754,7 +792,7 @@ void Problem::setup_precond(int kind, const oc_ipm_params& p)
             HF_.build_rediscretized(ctx, F, b);
             Op9 FT = P.LT;
             FT.diag = mhat_.get();
-            HFT_.allocate(level_);
+            HFT_.allocate(level_, 1, smoother_);
             HFT_.build_rediscretized(ctx, FT, bt);
         } else {
             HF_.build(ctx, F);

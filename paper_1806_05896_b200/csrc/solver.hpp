@@ -132,7 +132,8 @@ struct MgParams {
 // operator, or for `batch` operators of the same level (heat time blocks).
 class Hierarchy {
 public:
-    void allocate(int level, int batch = 1);
+    // smoother: OC_SMOOTHER_COLOR4 or OC_SMOOTHER_LEX (reference order, in place)
+    void allocate(int level, int batch = 1, int smoother = OC_SMOOTHER_COLOR4);
     // Galerkin coarse operators R A P of the fine operator (per batch block the
     // fine coef/diag pointers advance by fine_coef_stride / fine_diag_stride).
     void build(Ctx& c, const Op9& fine, long long fine_coef_stride = 0,
@@ -146,6 +147,7 @@ public:
     void smooth(Ctx& c, const double* b, double* x, bool forward, int bt);
     int depth() const { return K_; }
     int level() const { return level_; }
+    int smoother() const { return smoother_; }
     Op9 level_op(int k, int bt) const;
     long long level_n(int k) const { return (long long)nx_[k] * nx_[k]; }
 
@@ -156,7 +158,9 @@ private:
     void build_inv(Ctx& c);
     const double* inv_at(int k, int bt) const { return inv_[k].get() + (size_t)bt * level_n(k); }
 
-    int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1;
+    int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1, smoother_ = OC_SMOOTHER_COLOR4;
+    bool lex_ = false;     // lexicographic smoother: in-place wavefront sweeps, single-CTA bottom
+    DVec mbox_;            // wavefront hand-off mailbox (lex), ceil(nx/32) * nx sentinels
     bool cluster_ = false;  // bottom levels run in the 16-CTA cluster kernel
     std::vector<int> nx_;
     Op9 fine_{};
@@ -230,6 +234,7 @@ private:
     DVec t_, t2_, t3_, tf_, rblk_;
     Hierarchy HF_, HFT_, HL_, Hleft_, Hright_, Hheat_;
     bool HL_built_ = false;
+    int smoother_ = OC_SMOOTHER_COLOR4;
     int setup_kind_ = -1;
     // Krylov
     std::vector<DVec> V_, Z_;

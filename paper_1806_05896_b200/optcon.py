@@ -167,6 +167,19 @@ class ControlProblem:
     observation: Optional[Sequence[float]] = None  # (a1, b1, a2, b2)
 
 
+SMOOTHERS = {"color4": 0, "lex": 1}
+
+
+def smoother_id(s) -> int:
+    """'color4' (4-colour symmetric GS, default) or 'lex' (the reference's
+    lexicographic GS, multigrid.cpp:44-66, faithful mode); ints pass through."""
+    if isinstance(s, str):
+        if s not in SMOOTHERS:
+            raise OptconInvalidArgument(f"unknown smoother: {s}")
+        return SMOOTHERS[s]
+    return int(s)
+
+
 @dataclass
 class IpmParams:
     """ipm.hpp:17-32 (+ gmres_restart, smoother)."""
@@ -185,7 +198,7 @@ class IpmParams:
     mg_pre: int = 5
     mg_post: int = 5
     solver: str = "gmres-pt"
-    smoother: int = 0
+    smoother: object = "color4"  # or "lex"
     gmres_restart: int = 0
 
     def c(self) -> _lib.IpmParamsC:
@@ -195,7 +208,7 @@ class IpmParams:
             self.alpha0, self.sigma, self.eps_p, self.eps_d, self.eps_c, self.mu0,
             int(self.max_iterations), self.linear_tol, int(self.linear_maxit),
             int(self.cheb_steps), int(self.mg_cycles), int(self.mg_pre), int(self.mg_post),
-            SOLVERS[self.solver], int(self.smoother), int(self.gmres_restart))
+            SOLVERS[self.solver], smoother_id(self.smoother), int(self.gmres_restart))
 
 
 @dataclass
@@ -487,7 +500,7 @@ class MgHierarchy:
     """multigrid.hpp:43-64 over an explicit 9-point operator (9 x n arrays)."""
 
     def __init__(self, coef9, level: int, rediscretize: int = 0, eps: float = 0.1,
-                 ctx: Optional[Context] = None):
+                 ctx: Optional[Context] = None, smoother="color4"):
         self.ctx = ctx or default_context()
         self._L = self.ctx._L
         self.level = level
@@ -495,7 +508,8 @@ class MgHierarchy:
         a = _Arg()
         h = C.c_void_p()
         _lib.check(self._L.oc_mg_create(self.ctx.h, level, a.ptr(np.ravel(coef9), 9 * self.n),
-                                        rediscretize, C.c_double(eps), C.byref(h)))
+                                        rediscretize, C.c_double(eps), smoother_id(smoother),
+                                        C.byref(h)))
         self.h = h
 
     def __del__(self):

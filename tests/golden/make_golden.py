@@ -5,7 +5,8 @@ built by `make -C oracle`) on seeded inputs and stores inputs + outputs as
 small .npz files. GPU tests compare against these when the oracle library is
 not available on the box; CPU tests check the numpy restatement against them.
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            # everything
+    python tests/golden/make_golden.py NAME ...   # only these IPM cases
 """
 from __future__ import annotations
 
@@ -44,6 +45,12 @@ IPM_CASES = [
                         tau=1.0 / 16), dict(solver="gmres-pt", sigma=0.2)),
     ("smoke_l5", dict(pde="poisson", level=5, alpha=1e-2, beta=1e-3, u_a=-2.0, u_b=2.0),
      dict(solver="gmres-pt", sigma=0.2)),
+    # C3 in the capped-Krylov regime (every GMRES solve stops at linear_maxit,
+    # as C3 does at 1025^2 with maxit 200): the solution depends on the exact
+    # preconditioner, i.e. on the lexicographic smoother
+    ("c3_l6_capped", dict(pde="poisson", level=6, alpha=1e-4, beta=1e-3, u_a=-2.0, u_b=2.0,
+                          y_a=-0.2, y_b=0.3, obs=(0.0, 0.5, 0.0, 1.0)),
+     dict(solver="gmres-ppi", sigma=0.2, linear_maxit=15)),
 ]
 
 
@@ -65,8 +72,10 @@ def ref_problem(kw):
     return ref.RefProblem(pde, level, y_d=desired(kw), **k)
 
 
-def make_ipm():
+def make_ipm(only=()):
     for name, pkw, skw in IPM_CASES:
+        if only and name not in only:
+            continue
         P = ref_problem(pkw)
         r = P.solve(**skw)
         rec = np.array([[d["k"], d["mu"], d["norm_xp"], d["norm_xd"], d["norm_xc"],
@@ -121,6 +130,9 @@ def make_assembly():
 
 
 if __name__ == "__main__":
-    make_assembly()
-    make_kkt()
-    make_ipm()
+    if len(sys.argv) > 1:
+        make_ipm(tuple(sys.argv[1:]))
+    else:
+        make_assembly()
+        make_kkt()
+        make_ipm()

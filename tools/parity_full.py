@@ -63,7 +63,7 @@ def run_ref(args):
                       lin_converged=all(d["lin_converged"] for d in r.records[1:]))
 
 
-def run_gpu(cases):
+def run_gpu(cases, smoother="color4"):
     from paper_1806_05896_b200 import optcon as oc
 
     ctx = oc.Context(0)
@@ -75,7 +75,7 @@ def run_gpu(cases):
             kw["observation"] = c.obs
         qp = oc.QpProblem(oc.ControlProblem(**kw), oc.Grid(c.level), ctx)
         r = oc.ipm_solve(qp, oc.IpmParams(sigma=c.sigma, solver=c.solver,
-                                          gmres_restart=c.gmres_restart))
+                                          gmres_restart=c.gmres_restart, smoother=smoother))
         out[name] = dict(u=r.u.copy(), y=r.state.y.copy(), z=r.state.z.copy(), nli=r.stats.nli,
                          av_li=r.stats.av_li, objective=r.objective, converged=r.stats.converged,
                          ms=r.solve_ms, lin=[i.lin_iters for i in r.stats.iterations[1:]],
@@ -114,9 +114,10 @@ def main():
     ap.add_argument("cases", nargs="*", default=["C1", "C2", "C4", "C5", "C3@8"])
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "parity_full.json"))
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 4)
+    ap.add_argument("--smoother", default="color4", help="color4 | lex (faithful mode)")
     a = ap.parse_args()
     cases = case_list(a.cases)
-    gpu = run_gpu(cases)
+    gpu = run_gpu(cases, a.smoother)
     print("gpu done", {k: round(v["ms"], 1) for k, v in gpu.items()}, flush=True)
     report = {}
     ctx = mp.get_context("fork")
@@ -124,6 +125,8 @@ def main():
         for name, r in pool.imap_unordered(run_ref, cases):
             c = dict(cases)[name]
             report[name] = compare(c, gpu[name], r)
+            report[name]["smoother"] = a.smoother
+            report[name]["lin_iters"] = (gpu[name]["lin"], r["lin"])
             print(name, json.dumps(report[name]), flush=True)
             os.makedirs(os.path.dirname(a.out), exist_ok=True)
             json.dump(report, open(a.out, "w"), indent=1)

@@ -1,7 +1,7 @@
 """Run the BASELINE configs C1..C5 at full size on the device and print
 time-to-tolerance and iteration statistics (one JSON line per config).
 
-    python tools/run_configs.py [C1 C2 C3 C4 C5]
+    python tools/run_configs.py [--smoother lex] [C1 C2 C3 C4 C5]
 """
 import json
 import os
@@ -13,7 +13,11 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1806_05896_b200 import configs, optcon as oc  # noqa: E402
 
-names = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
+args = sys.argv[1:]
+smoother = "color4"
+if args[:1] == ["--smoother"]:
+    smoother, args = args[1], args[2:]
+names = args or ["C1", "C2", "C3", "C4", "C5"]
 ctx = oc.Context(0)
 for name in names:
     c = configs.ALL[name]
@@ -29,7 +33,8 @@ for name in names:
     t0 = time.perf_counter()
     qp = oc.QpProblem(oc.ControlProblem(**kw), oc.Grid(c.level), ctx)
     t_setup = time.perf_counter() - t0
-    params = oc.IpmParams(sigma=c.sigma, solver=c.solver, gmres_restart=c.gmres_restart)
+    params = oc.IpmParams(sigma=c.sigma, solver=c.solver, gmres_restart=c.gmres_restart,
+                          smoother=smoother)
     t0 = time.perf_counter()
     try:
         r = oc.ipm_solve(qp, params)
@@ -38,7 +43,7 @@ for name in names:
         continue
     wall = time.perf_counter() - t0
     print(json.dumps({
-        "config": name, "level": c.level, "solver": c.solver, "setup_s": round(t_setup, 3),
+        "config": name, "level": c.level, "solver": c.solver, "smoother": smoother, "setup_s": round(t_setup, 3),
         "solve_ms": round(r.solve_ms, 2), "wall_s": round(wall, 3), "nli": r.stats.nli,
         "av_li": round(r.stats.av_li, 3), "converged": r.stats.converged,
         "lin_iters": [i.lin_iters for i in r.stats.iterations[1:]],
