@@ -56,7 +56,10 @@ struct SweepShape {
     static constexpr int H = 4 * NS;
     static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
     static constexpr int R = RX * RY;
-    static constexpr int PLANES = VAR ? 11 : 3; // x, b, inv (+ 8 off-diagonals)
+    // variable coefficients are staged for single sweeps; fused sweeps read
+    // them through L1 (the region grows with NS, the coefficient planes would not fit)
+    static constexpr bool CS = VAR && NS == 1;
+    static constexpr int PLANES = CS ? 11 : 3; // x, b, inv (+ 8 off-diagonals)
     static constexpr size_t smem = (size_t)PLANES * R * sizeof(double);
 };
 
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 else cp_async8(xs + l, xin + i);
                 cp_async8(bs + l, b + i);
                 cp_async8(iv + l, inv + i);
-                if (VAR) {
+                if (S::CS) {
 #pragma unroll
                     for (int p = 0; p < 8; ++p) cp_async8(cs + p * R + l, A.coef + (p < 4 ? p : p + 1) * n + i);
                 }
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 xs[l] = 0.0;
                 bs[l] = 0.0;
                 iv[l] = 0.0;
-                if (VAR) {
+                if (S::CS) {
 #pragma unroll
                     for (int p = 0; p < 8; ++p) cs[p * R + l] = 0.0;
                 }
@@ -140,11 +143,13 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         for (int gy = gy0 + 2 * ty; gy < hiy; gy += 16) {
             for (int gx = gx0 + 2 * tx; gx < hix; gx += 64) {
                 const int l = (gy - oy) * RX + (gx - ox);
+                const long long gi = (long long)gy * nx + gx;
                 double s = bs[l];
 #pragma unroll
                 for (int d = 0; d < 9; ++d) {
                     if (d == 4) continue;
-                    const double a = VAR ? cs[(d < 4 ? d : d - 1) * R + l] : A.c[d];
+                    const double a = S::CS ? cs[(d < 4 ? d : d - 1) * R + l]
+                                           : (VAR ? __ldg(A.coef + d * n + gi) : A.c[d]);
                     s -= a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
                 }
                 xs[l] = s * iv[l];
@@ -291,6 +296,23 @@ void sweep_pick_var(cudaStream_t s, const Op9& A, const double* b, const double*
     else sweep_go<TX, TY, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec);
 }
 
+template <int NS>
+void sweep_tile(int id, cudaStream_t s, const Op9& A, const double* b, const double* inv,
+                const double* x, double* xo, bool forward, bool zero_init, const double* ec)
+{
+    switch (id) {
+    case 0:
+        if constexpr (NS <= 2) {
+            sweep_go<64, 32, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec);
+            break;
+        }
+        [[fallthrough]];
+    case 1: sweep_pick_var<32, 32, NS>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    case 2: sweep_pick_var<32, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    default: sweep_pick_var<16, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    }
+}
+
 } // namespace
 
 int g_sweep_tile = -1; // tuning override: -1 auto, else tile id (see launch_sweep_tiled)
@@ -310,21 +332,13 @@ void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const dou
 {
     int id = g_sweep_tile;
     if (id < 0) id = A.nx >= 1000 ? 1 : (A.nx >= 500 ? 2 : 3);
-    if (A.coef && id == 0) id = 1; // 64x32 variable tiles exceed shared memory
-    if (ns == 2) {
-        switch (id) {
-        case 0: sweep_go<64, 32, 2, false>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-        case 1: sweep_pick_var<32, 32, 2>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-        case 2: sweep_pick_var<32, 16, 2>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-        default: sweep_pick_var<16, 16, 2>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-        }
-        return;
-    }
-    switch (id) {
-    case 0: sweep_go<64, 32, 1, false>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    case 1: sweep_pick_var<32, 32, 1>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    case 2: sweep_pick_var<32, 16, 1>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    default: sweep_pick_var<16, 16, 1>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    if (id == 0 && (A.coef || ns > 2)) id = 1; // 64x32 tiles: constant stencils, <= 2 sweeps
+    switch (ns) {
+    case 1: sweep_tile<1>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    case 2: sweep_tile<2>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    case 3: sweep_tile<3>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    case 4: sweep_tile<4>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    default: sweep_tile<5>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
     }
 }
 

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <atomic>
 #include <mutex>
+#include <cstdlib>
 #include <cstring>
 
 namespace ocb {
@@ -53,6 +54,7 @@ void pool_free(void* p)
 
 static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int Profiler::begin(cudaStream_t s, int cat)
@@ -146,6 +148,7 @@ void Hierarchy::allocate(int level, int batch, int smoother)
     if (smoother != OC_SMOOTHER_COLOR4 && smoother != OC_SMOOTHER_LEX)
         throw InvalidArgument("MgHierarchy: unknown smoother");
     if (built_ && level == level_ && batch == batch_ && smoother == smoother_) return;
+    ++gen_;
     level_ = level;
     batch_ = batch;
     smoother_ = smoother;
@@ -305,7 +308,7 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
     double* Abuf = xout;
     double* Bbuf = xb_[k].get();
     // sweeps are fused g_sweep_fuse at a time (same colour-pass sequence)
-    const int F = g_sweep_fuse < 1 ? 1 : (g_sweep_fuse > 2 ? 2 : g_sweep_fuse);
+    const int F = g_sweep_fuse < 1 ? 1 : (g_sweep_fuse > 5 ? 5 : g_sweep_fuse);
     const int Lpre = (p.pre + F - 1) / F, Lpost = (p.post + F - 1) / F;
     const int S = Lpre + Lpost; // out-of-place launches; the last one must land in xout
     auto outbuf = [&](int s) { return ((S - s) % 2 == 0) ? Abuf : Bbuf; };
@@ -834,7 +837,84 @@ void Problem::time_schur(const double* r, double* out)
     }
 }
 
+Problem::~Problem()
+{
+    cudaStreamSynchronize(ctx.stream);
+    drop_graphs();
+}
+
+void Problem::drop_graphs()
+{
+    for (auto& kv : graphs_)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs_.clear();
+}
+
+long long Problem::hierarchy_generation() const
+{
+    return HF_.generation() + HFT_.generation() + HL_.generation() + Hleft_.generation() +
+           Hright_.generation() + Hheat_.generation();
+}
+
 void Problem::precond_apply(int kind, const double* r, double* out)
+{
+    static const bool env_off = [] {
+        const char* e = getenv("OC_GRAPHS");
+        return e && e[0] == '0';
+    }();
+    if (env_off || !graphs_enabled_ || ctx.prof.on) {
+        precond_apply_direct(kind, r, out);
+        return;
+    }
+    // the argument checks of precond_apply_direct, which a replay would skip
+    if (setup_kind_ < 0) throw InvalidArgument("preconditioner not set up");
+    if (kind == OC_PRECOND_PPI) {
+        if (heat_) throw InvalidArgument("gmres-ppi is not available for heat problems");
+        if (setup_kind_ != OC_PRECOND_PPI) throw InvalidArgument("P_Pi not set up");
+    } else if (setup_kind_ == OC_PRECOND_PPI && !heat_) {
+        throw InvalidArgument("P_D/P_T not set up");
+    }
+    const long long gen = hierarchy_generation();
+    if (gen != graph_gen_) {
+        drop_graphs();
+        graph_gen_ = gen;
+    }
+    GraphKey key{kind, r, out, mg_.cycles, mg_.pre, mg_.post, cheb_steps_};
+    GraphEntry& g = graphs_[key];
+    if (g.exec) {
+        cuda_check(cudaGraphLaunch(g.exec, ctx.stream), "cudaGraphLaunch");
+        add_launches(g.launches);
+        return;
+    }
+    if (++g.uses < 2) { // first use runs directly (also performs one-time kernel setup)
+        precond_apply_direct(kind, r, out);
+        return;
+    }
+    const long long l0 = launch_count();
+    cudaGraph_t graph = nullptr;
+    cuda_check(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal),
+               "cudaStreamBeginCapture");
+    try {
+        precond_apply_direct(kind, r, out);
+    } catch (...) {
+        cudaStreamEndCapture(ctx.stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    cuda_check(cudaStreamEndCapture(ctx.stream, &graph), "cudaStreamEndCapture");
+    const long long captured = launch_count() - l0;
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cuda_check(e, "cudaGraphInstantiate");
+    g.exec = exec;
+    g.launches = captured;
+    add_launches(-captured); // the captured launches did not run; the replay does
+    cuda_check(cudaGraphLaunch(exec, ctx.stream), "cudaGraphLaunch");
+    add_launches(captured);
+}
+
+void Problem::precond_apply_direct(int kind, const double* r, double* out)
 {
     if (setup_kind_ < 0) throw InvalidArgument("preconditioner not set up");
     const long long N = ny_;
@@ -1315,8 +1395,9 @@ void Problem::time_applies(int kind, int reps, double* kkt_ms, double* prec_ms)
     kw_.resize(n);
     kx2_.resize(n);
     launch_fill(ctx.stream, kx2_.get(), 1.0, n);
-    // warm-up
+    // warm-up (two preconditioner applies: the second one captures its graph)
     kkt(kx2_.get(), kw_.get());
+    precond_apply(kind, kx2_.get(), kw_.get());
     precond_apply(kind, kx2_.get(), kw_.get());
     ctx.sync();
     cudaEventRecord(ctx.ev0, ctx.stream);

@@ -8,7 +8,9 @@
 #include "../../include/optcon_b200.h"
 #include "kernels.hpp"
 
+#include <map>
 #include <memory>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -148,6 +150,9 @@ public:
     int depth() const { return K_; }
     int level() const { return level_; }
     int smoother() const { return smoother_; }
+    // bumped whenever allocate() (re)allocates device buffers: captured graphs
+    // that bake in this hierarchy's pointers are then stale
+    long long generation() const { return gen_; }
     Op9 level_op(int k, int bt) const;
     long long level_n(int k) const { return (long long)nx_[k] * nx_[k]; }
 
@@ -160,6 +165,7 @@ private:
 
     int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1, smoother_ = OC_SMOOTHER_COLOR4;
     bool lex_ = false;     // lexicographic smoother: in-place wavefront sweeps, single-CTA bottom
+    long long gen_ = 0;
     DVec mbox_;            // wavefront hand-off mailbox (lex), ceil(nx/32) * nx sentinels
     bool cluster_ = false;  // bottom levels run in the 16-CTA cluster kernel
     std::vector<int> nx_;
@@ -179,12 +185,13 @@ private:
 class Problem {
 public:
     Problem(Ctx& c, const oc_problem_desc& d);
-    ~Problem() { cudaStreamSynchronize(ctx.stream); } // before members return memory to the pool
+    ~Problem(); // synchronises before members return memory to the pool
     oc_problem_info info() const;
 
     // preconditioner setup from Theta already in ty_/tw_/tv_ (device)
     void setup_precond(int kind, const oc_ipm_params& p);
     void precond_apply(int kind, const double* r, double* out);
+    void precond_apply_direct(int kind, const double* r, double* out);
     void schur_apply(const double* r, double* out);
     void kkt(const double* x, double* out);
     void set_theta(const double* ty, const double* tw, const double* tv);
@@ -236,6 +243,22 @@ private:
     bool HL_built_ = false;
     int smoother_ = OC_SMOOTHER_COLOR4;
     int setup_kind_ = -1;
+    // CUDA graphs of the preconditioner apply, keyed by (kind, r, out, MG and
+    // Chebyshev parameters): captured on the second use of a key, replayed
+    // afterwards (one launch instead of ~200). Device pointers baked into the
+    // graphs are stable across Newton steps; any hierarchy reallocation (see
+    // Hierarchy::generation) drops them.
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        int uses = 0;
+        long long launches = 0;
+    };
+    using GraphKey = std::tuple<int, const void*, const void*, int, int, int, int>;
+    std::map<GraphKey, GraphEntry> graphs_;
+    long long graph_gen_ = -1;
+    bool graphs_enabled_ = true;
+    void drop_graphs();
+    long long hierarchy_generation() const;
     // Krylov
     std::vector<DVec> V_, Z_;
     DevArray<const double*> Ztab_;

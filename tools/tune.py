@@ -18,7 +18,7 @@ qp = oc.build_qp(oc.ControlProblem(alpha=c.alpha, beta=c.beta, y_d=c.y_d(), u_a=
 params = oc.IpmParams(sigma=0.2, solver=solver)
 oc.ipm_solve(qp, params)
 ref_u = None
-for fuse in (1, 2):
+for fuse in (1, 2, 3, 5):
     for tile in (0, 1, 2, 3):
         L.oc_set_tuning(b"sweep_tile", tile)
         L.oc_set_tuning(b"sweep_fuse", fuse)
