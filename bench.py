@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--level", type=int, default=9)
     ap.add_argument("--solver", default="gmres-pt")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep-fuse", type=int, default=None,
+                    help="smoothing sweeps fused per tiled launch (1..5; library default if unset)")
+    ap.add_argument("--sweep-tile", type=int, default=None, help="tiled sweep shape id (tuning)")
     return ap.parse_args()
 
 
@@ -209,8 +212,12 @@ def measured_peak_hbm():
 def run_ours(args):
     import torch
 
-    from paper_1806_05896_b200 import bytes_model, optcon as oc
+    from paper_1806_05896_b200 import _lib, bytes_model, optcon as oc
 
+    if args.sweep_fuse is not None:
+        _lib.check(_lib.load().oc_set_tuning(b"sweep_fuse", int(args.sweep_fuse)))
+    if args.sweep_tile is not None:
+        _lib.check(_lib.load().oc_set_tuning(b"sweep_tile", int(args.sweep_tile)))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

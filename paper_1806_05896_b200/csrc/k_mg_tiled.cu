@@ -316,7 +316,7 @@ void sweep_tile(int id, cudaStream_t s, const Op9& A, const double* b, const dou
 } // namespace
 
 int g_sweep_tile = -1; // tuning override: -1 auto, else tile id (see launch_sweep_tiled)
-int g_sweep_fuse = 1;  // sweeps fused per launch
+int g_sweep_fuse = 2;  // sweeps fused per launch (measured best, profiles/r01/tuning.md)
 
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
                      long long fds)
@@ -331,7 +331,15 @@ void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const dou
                         const double* ec, int ns)
 {
     int id = g_sweep_tile;
-    if (id < 0) id = A.nx >= 1000 ? 1 : (A.nx >= 500 ? 2 : 3);
+    if (id < 0) {
+        // Alone on the GPU a sweep is latency-bound: prefer more, smaller tiles.
+        // With several solves in flight (one context each) the sweeps compete
+        // for bandwidth: prefer the larger tiles (less halo re-read).
+        const bool shared = active_contexts() > 1;
+        if (A.nx >= 1000) id = 1;
+        else if (A.nx >= 500) id = shared ? (A.coef ? 1 : 0) : 2;
+        else id = (shared && A.coef) ? 1 : 3;
+    }
     if (id == 0 && (A.coef || ns > 2)) id = 1; // 64x32 tiles: constant stencils, <= 2 sweeps
     switch (ns) {
     case 1: sweep_tile<1>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;

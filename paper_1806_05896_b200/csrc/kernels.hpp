@@ -8,6 +8,7 @@ namespace ocb {
 
 // Count of kernel launches issued by this library (bench "gpu_launches").
 void note_launch();
+int active_contexts(); // live oc_ctx objects in this process (tile-shape heuristic)
 void add_launches(long long k); // graph replays count their kernel nodes
 long long launch_count();
 

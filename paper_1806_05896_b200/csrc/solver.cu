@@ -53,7 +53,14 @@ void pool_free(void* p)
 }
 
 static std::atomic<long long> g_launches{0};
-void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static thread_local long long t_launches = 0; // this host thread's launches (graph capture)
+void note_launch()
+{
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    ++t_launches;
+}
+static std::atomic<int> g_contexts{0};
+int active_contexts() { return g_contexts.load(std::memory_order_relaxed); }
 void add_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
@@ -108,10 +115,12 @@ Ctx::Ctx(int dev) : device(dev)
     for (auto& e : user_ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     cuda_check(cudaMallocHost(&hscal, 64 * sizeof(double)), "cudaMallocHost");
     cuda_check(cudaMallocHost(&hflags, 8 * sizeof(int)), "cudaMallocHost");
+    g_contexts.fetch_add(1, std::memory_order_relaxed);
 }
 
 Ctx::~Ctx()
 {
+    g_contexts.fetch_sub(1, std::memory_order_relaxed);
     if (stream) cudaStreamSynchronize(stream);
     if (hscal) cudaFreeHost(hscal);
     if (hflags) cudaFreeHost(hflags);
@@ -879,7 +888,8 @@ void Problem::precond_apply(int kind, const double* r, double* out)
         drop_graphs();
         graph_gen_ = gen;
     }
-    GraphKey key{kind, r, out, mg_.cycles, mg_.pre, mg_.post, cheb_steps_};
+    // (launch-shape tuning knobs are part of the key: they change the captured launches)
+    GraphKey key{kind, r, out, mg_.cycles, mg_.pre, mg_.post, cheb_steps_, g_sweep_tile, g_sweep_fuse};
     GraphEntry& g = graphs_[key];
     if (g.exec) {
         cuda_check(cudaGraphLaunch(g.exec, ctx.stream), "cudaGraphLaunch");
@@ -890,7 +900,7 @@ void Problem::precond_apply(int kind, const double* r, double* out)
         precond_apply_direct(kind, r, out);
         return;
     }
-    const long long l0 = launch_count();
+    const long long l0 = t_launches; // other threads launch concurrently: count our own
     cudaGraph_t graph = nullptr;
     cuda_check(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal),
                "cudaStreamBeginCapture");
@@ -902,7 +912,7 @@ void Problem::precond_apply(int kind, const double* r, double* out)
         throw;
     }
     cuda_check(cudaStreamEndCapture(ctx.stream, &graph), "cudaStreamEndCapture");
-    const long long captured = launch_count() - l0;
+    const long long captured = t_launches - l0;
     cudaGraphExec_t exec = nullptr;
     const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);

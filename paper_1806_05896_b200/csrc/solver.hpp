@@ -253,7 +253,7 @@ private:
         int uses = 0;
         long long launches = 0;
     };
-    using GraphKey = std::tuple<int, const void*, const void*, int, int, int, int>;
+    using GraphKey = std::tuple<int, const void*, const void*, int, int, int, int, int, int>;
     std::map<GraphKey, GraphEntry> graphs_;
     long long graph_gen_ = -1;
     bool graphs_enabled_ = true;

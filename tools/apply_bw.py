@@ -11,14 +11,19 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1806_05896_b200 import bytes_model, configs, optcon as oc  # noqa: E402
+from paper_1806_05896_b200 import _lib, bytes_model, configs, optcon as oc  # noqa: E402
 
 KIND = {"gmres-pt": "pt", "minres-pd": "pd", "gmres-ppi": "ppi"}
 
 args = sys.argv[1:]
 smoother = "color4"
-if args[:1] == ["--smoother"]:
-    smoother, args = args[1], args[2:]
+while args[:1] and args[0].startswith("--"):
+    flag, val, args = args[0], args[1], args[2:]
+    if flag == "--smoother":
+        smoother = val
+    elif flag in ("--fuse", "--tile"):
+        key = b"sweep_fuse" if flag == "--fuse" else b"sweep_tile"
+        _lib.check(_lib.load().oc_set_tuning(key, int(val)))
 names = args or ["C1", "C2", "C4", "C5", "C3"]
 peak = None
 try:

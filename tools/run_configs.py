@@ -11,12 +11,17 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1806_05896_b200 import configs, optcon as oc  # noqa: E402
+from paper_1806_05896_b200 import _lib, configs, optcon as oc  # noqa: E402
 
 args = sys.argv[1:]
 smoother = "color4"
-if args[:1] == ["--smoother"]:
-    smoother, args = args[1], args[2:]
+while args[:1] and args[0].startswith("--"):
+    flag, val, args = args[0], args[1], args[2:]
+    if flag == "--smoother":
+        smoother = val
+    elif flag in ("--fuse", "--tile"):
+        key = b"sweep_fuse" if flag == "--fuse" else b"sweep_tile"
+        _lib.check(_lib.load().oc_set_tuning(key, int(val)))
 names = args or ["C1", "C2", "C3", "C4", "C5"]
 ctx = oc.Context(0)
 for name in names:
