@@ -382,9 +382,53 @@ __device__ void bt_sweep(const Op9& A, const double* bsm, double* xsm, bool forw
 
 // Lexicographic sweep of one bottom level in shared memory (lex_gs.cuh): warps
 // 0..ceil(nx/32)-1 run the skewed wavefront; the hand-off between them goes
-// through the shared mailbox mbs (sentinel-filled, restored on return).
-__device__ void bt_sweep_lex(const Op9& A, const double* bsm, double* xsm, volatile double* mbs,
-                             bool fwd)
+// through the shared mailbox mbs (sentinel-filled, restored on return). The
+// operands of a column (b, old E/NW/N/NE, 1/a_ii from shared memory; the
+// coefficients of variable operators from global memory, prefetched into L1)
+// are loaded kBtLexR steps ahead into a register ring, so a step's dependent
+// chain is the shuffle plus the FMAs of the update.
+constexpr int kBtLexR = 4;
+constexpr int kBtLexPF = 0; // L1 prefetch distance (0: off)
+
+struct BtRaw {
+    double b, e, nw, nn, ne, inv;
+    double a[8];
+};
+
+__device__ __forceinline__ void bt_lex_load(BtRaw& p, const Op9& A, const double* bsm,
+                                            const double* xsm, const double* ism, long long n,
+                                            int row0, int sx, int sy, int nx, bool rowok,
+                                            bool hasN, bool fwd, int col)
+{
+    p.b = p.e = p.nw = p.nn = p.ne = p.inv = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p.a[k] = 0.0;
+    if (!rowok || col < 0 || col >= nx) return;
+    const int i = row0 + col * sx;
+    const bool hasE = col + 1 < nx, hasW = col > 0;
+    if (kBtLexPF > 0 && A.coef && col + kBtLexPF < nx) {
+#pragma unroll
+        for (int d = 0; d < 9; ++d)
+            if (d != 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.coef + d * n + i + kBtLexPF * sx));
+    }
+    if (hasE) p.e = xsm[i + sx];
+    if (hasN) {
+        p.nn = xsm[i + sy];
+        if (hasW) p.nw = xsm[i + sy - sx];
+        if (hasE) p.ne = xsm[i + sy + sx];
+    }
+    p.b = bsm[i];
+    p.inv = ism[i];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int d = k < 4 ? k : k + 1;
+        const int dp = fwd ? d : 8 - d;
+        p.a[k] = A.coef ? __ldg(A.coef + dp * n + i) : A.c[dp];
+    }
+}
+
+__device__ void bt_sweep_lex(const Op9& A, const double* bsm, double* xsm, const double* ism,
+                             volatile double* mbs, bool fwd)
 {
     const int nx = A.nx;
     const long long n = (long long)nx * nx;
@@ -398,43 +442,56 @@ __device__ void bt_sweep_lex(const Op9& A, const double* bsm, double* xsm, volat
         const bool consumer = j == 0 && wid > 0, producer = j == 31 && hasN;
         volatile double* mb_in = mbs + (wid > 0 ? wid - 1 : 0) * nx;
         volatile double* mb_out = mbs + wid * nx;
-        double sw = 0.0, s = 0.0, se = 0.0, last = 0.0, n_prev = 0.0;
-        for (int st = -1; st < nx + 62; ++st) {
-            const int xl = st - 2 * j;
+        auto receive = [&](int xe) -> double {
+            double v = mb_in[xe];
+            while (lex_is_sentinel(v)) v = mb_in[xe];
+            mb_in[xe] = lex_sentinel();
+            return v;
+        };
+        double sw = 0.0, s = 0.0, se = 0.0, last = 0.0;
+        {   // step -1: lane 0 primes its window with column 0 of row r-1
             double up = __shfl_up_sync(0xffffffffu, last, 1);
-            if (j == 0) {
-                up = 0.0;
-                const int xe = st + 1;
-                if (consumer && xe < nx) {
-                    double v = mb_in[xe];
-                    while (lex_is_sentinel(v)) v = mb_in[xe];
-                    up = v;
-                    mb_in[xe] = lex_sentinel();
-                }
-            }
-            sw = s;
-            s = se;
+            if (j == 0) up = consumer ? receive(0) : 0.0;
             se = up;
-            double v = 0.0, nn = 0.0;
-            if (rowok && xl >= 0 && xl < nx) {
-                const int i = row0 + xl * sx;
-                const bool hasE = xl + 1 < nx;
-                const double e = hasE ? xsm[i + sx] : 0.0;
-                double ne = 0.0;
-                if (hasN) {
-                    nn = xsm[i + sy];
-                    if (hasE) ne = xsm[i + sy + sx];
+        }
+        BtRaw ring[kBtLexR];
+#pragma unroll
+        for (int u = 0; u < kBtLexR; ++u)
+            bt_lex_load(ring[u], A, bsm, xsm, ism, n, row0, sx, sy, nx, rowok, hasN, fwd, u - 2 * j);
+        const int nsteps = nx + 62;
+        for (int base = 0; base < nsteps; base += kBtLexR) {
+#pragma unroll
+            for (int u = 0; u < kBtLexR; ++u) {
+                const int st = base + u;
+                const int xl = st - 2 * j;
+                const BtRaw& p = ring[u];
+                double t = p.b;
+                t -= p.a[4] * p.e;
+                t -= p.a[5] * p.nw;
+                t -= p.a[6] * p.nn;
+                t -= p.a[7] * p.ne;
+                double up = __shfl_up_sync(0xffffffffu, last, 1);
+                if (j == 0) {
+                    const int xe = st + 1;
+                    up = (consumer && xe < nx) ? receive(xe) : 0.0;
                 }
-                auto a = [&](int d) -> double {
-                    const int dp = fwd ? d : 8 - d;
-                    return A.coef ? A.coef[dp * n + i] : A.c[dp];
-                };
-                v = lex_update(a, bsm[i], 1.0 / diag_at(A, i, n), sw, s, se, last, e, n_prev, nn, ne);
-                xsm[i] = v;
-                if (producer) mb_out[xl] = v;
+                sw = s;
+                s = se;
+                se = up;
+                double v = 0.0;
+                if (rowok && xl >= 0 && xl < nx) {
+                    t -= p.a[0] * sw;
+                    t -= p.a[1] * s;
+                    t -= p.a[2] * se;
+                    t -= p.a[3] * last;
+                    v = t * p.inv;
+                    xsm[row0 + xl * sx] = v;
+                    if (producer) mb_out[xl] = v;
+                }
+                last = v;
+                bt_lex_load(ring[u], A, bsm, xsm, ism, n, row0, sx, sy, nx, rowok, hasN, fwd,
+                            xl + kBtLexR);
             }
-            n_prev = nn;
-            last = v;
         }
     }
     __syncthreads();
@@ -457,10 +514,12 @@ __device__ double bt_resid_sq(const Op9& A, const double* bsm, const double* xsm
     return out;
 }
 
-__global__ void __launch_bounds__(kBottomThreads) k_bottom(BottomArgs a, const double* __restrict__ bg,
-                                                           double* __restrict__ xg, int cycles,
-                                                           int pre, int post, int check,
-                                                           double* state, int* flags)
+// LEX: the reference's lexicographic smoother, run by 2 warps as a wavefront
+// (64-thread block: registers for the operand rings); else 4-colour, 1024 threads.
+template <bool LEX>
+__global__ void __launch_bounds__(LEX ? 64 : kBottomThreads)
+    k_bottom(BottomArgs a, const double* __restrict__ bg, double* __restrict__ xg, int cycles,
+             int pre, int post, int check, double* state, int* flags)
 {
     extern __shared__ double sm[];
     __shared__ double red[40];
@@ -475,7 +534,18 @@ __global__ void __launch_bounds__(kBottomThreads) k_bottom(BottomArgs a, const d
     double* rs = p;
     const int n0 = a.ops[0].nx * a.ops[0].nx;
     volatile double* mbs = rs + n0; // lexicographic hand-off mailbox (64 slots)
-    if (a.lex && threadIdx.x < 64) mbs[threadIdx.x] = lex_sentinel();
+    double* is_[kBottomMaxLevels];  // lexicographic mode: 1/a_ii per level
+    if (LEX) {
+        if (threadIdx.x < 64) mbs[threadIdx.x] = lex_sentinel();
+        double* q = rs + n0 + 64;
+        for (int k = 0; k < a.nlev; ++k) {
+            const Op9& A = a.ops[k];
+            const long long m = (long long)A.nx * A.nx;
+            is_[k] = q;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) q[i] = 1.0 / diag_at(A, i, m);
+            q += m;
+        }
+    }
     for (int i = threadIdx.x; i < n0; i += blockDim.x) {
         bs[0][i] = bg[i];
         xs[0][i] = 0.0;
@@ -497,7 +567,7 @@ __global__ void __launch_bounds__(kBottomThreads) k_bottom(BottomArgs a, const d
         for (int k = 0; k < last; ++k) {
             const Op9& A = a.ops[k];
             for (int s = 0; s < pre; ++s) {
-                if (a.lex) bt_sweep_lex(A, bs[k], xs[k], mbs, true);
+                if (LEX) bt_sweep_lex(A, bs[k], xs[k], is_[k], mbs, true);
                 else bt_sweep(A, bs[k], xs[k], true);
             }
             const int nx = A.nx, nxc = (nx - 1) / 2;
@@ -539,7 +609,7 @@ __global__ void __launch_bounds__(kBottomThreads) k_bottom(BottomArgs a, const d
                 xs[k][i] = xs[k][i] + prolong_at(xs[k + 1], nxc, i % nx, i / nx);
             __syncthreads();
             for (int s = 0; s < post; ++s) {
-                if (a.lex) bt_sweep_lex(A, bs[k], xs[k], mbs, false);
+                if (LEX) bt_sweep_lex(A, bs[k], xs[k], is_[k], mbs, false);
                 else bt_sweep(A, bs[k], xs[k], false);
             }
         }
@@ -638,6 +708,8 @@ size_t bottom_smem_bytes(const BottomArgs& a)
     for (int k = 0; k < a.nlev; ++k) m += 2ull * a.ops[k].nx * a.ops[k].nx;
     m += (size_t)a.ops[0].nx * a.ops[0].nx;
     m += 64; // lexicographic hand-off mailbox
+    if (a.lex)
+        for (int k = 0; k < a.nlev; ++k) m += (size_t)a.ops[k].nx * a.ops[k].nx; // 1/a_ii
     return m * sizeof(double);
 }
 
@@ -647,13 +719,17 @@ void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double*
     const size_t smem = bottom_smem_bytes(a);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bottom<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bottom<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     if (smem > 200 * 1024) throw std::runtime_error("bottom solver: level too large for one CTA");
     note_launch();
-    k_bottom<<<1, kBottomThreads, smem, s>>>(a, b, x, cycles, pre, post, check ? 1 : 0, state,
-                                             flags);
+    if (a.lex)
+        k_bottom<true><<<1, 64, smem, s>>>(a, b, x, cycles, pre, post, check ? 1 : 0, state, flags);
+    else
+        k_bottom<false><<<1, kBottomThreads, smem, s>>>(a, b, x, cycles, pre, post, check ? 1 : 0,
+                                                        state, flags);
 }
 
 } // namespace ocb
