@@ -30,24 +30,43 @@ __device__ __forceinline__ void cp_async_wait_all()
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+// (P ec)(gx, gy): bilinear prolongation, parents in ascending column order,
+// branch-free (weight 0 = absent parent; no local-memory arrays)
 __device__ __forceinline__ double prolong_at2(const double* __restrict__ ec, int nxc, int gx, int gy)
 {
-    int px[2], py[2];
-    double wx[2], wy[2];
-    int cxn = 0, cyn = 0;
-    if (gx & 1) { px[0] = (gx - 1) >> 1; wx[0] = 1.0; cxn = 1; }
-    else {
-        if (gx / 2 - 1 >= 0) { px[cxn] = gx / 2 - 1; wx[cxn++] = 0.5; }
-        if (gx / 2 < nxc) { px[cxn] = gx / 2; wx[cxn++] = 0.5; }
+    int x0, x1, y0, y1;
+    double wx0, wx1, wy0, wy1;
+    if (gx & 1) {
+        x0 = x1 = (gx - 1) >> 1;
+        wx0 = 1.0;
+        wx1 = 0.0;
+    } else {
+        x0 = gx / 2 - 1;
+        x1 = gx / 2;
+        wx0 = x0 >= 0 ? 0.5 : 0.0;
+        wx1 = x1 < nxc ? 0.5 : 0.0;
     }
-    if (gy & 1) { py[0] = (gy - 1) >> 1; wy[0] = 1.0; cyn = 1; }
-    else {
-        if (gy / 2 - 1 >= 0) { py[cyn] = gy / 2 - 1; wy[cyn++] = 0.5; }
-        if (gy / 2 < nxc) { py[cyn] = gy / 2; wy[cyn++] = 0.5; }
+    if (gy & 1) {
+        y0 = y1 = (gy - 1) >> 1;
+        wy0 = 1.0;
+        wy1 = 0.0;
+    } else {
+        y0 = gy / 2 - 1;
+        y1 = gy / 2;
+        wy0 = y0 >= 0 ? 0.5 : 0.0;
+        wy1 = y1 < nxc ? 0.5 : 0.0;
     }
     double e = 0.0;
-    for (int a = 0; a < cyn; ++a)
-        for (int c = 0; c < cxn; ++c) e += (wx[c] * wy[a]) * ec[(long long)py[a] * nxc + px[c]];
+    if (wy0 != 0.0) {
+        const double* r = ec + (long long)y0 * nxc;
+        if (wx0 != 0.0) e += (wx0 * wy0) * r[x0];
+        if (wx1 != 0.0) e += (wx1 * wy0) * r[x1];
+    }
+    if (wy1 != 0.0) {
+        const double* r = ec + (long long)y1 * nxc;
+        if (wx0 != 0.0) e += (wx0 * wy1) * r[x0];
+        if (wx1 != 0.0) e += (wx1 * wy1) * r[x1];
+    }
     return e;
 }
 
@@ -130,6 +149,25 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     }
     __syncthreads();
 
+    // Fixed node table: thread t owns colour-sub-lattice positions k = t + 256 m
+    // of the region (region origin ox, oy is even, so a colour's nodes are
+    // (2 kx + cx, 2 ky + cy) in region coordinates for every pass); shared
+    // offsets and global coordinates are computed once, neighbours are
+    // compile-time offsets from l.
+    constexpr int CXN = RX / 2, CYN = RY / 2, KC = CXN * CYN, KT = (KC + 255) / 256;
+    static_assert(RX % 2 == 0 && RY % 2 == 0, "even regions keep colour parity");
+    int kl[KT], kx0[KT], ky0[KT];
+#pragma unroll
+    for (int m = 0; m < KT; ++m) {
+        const int k = threadIdx.x + 256 * m;
+        const int ky = k / CXN, kx = k - ky * CXN;
+        kl[m] = 2 * ky * RX + 2 * kx;
+        kx0[m] = k < KC ? ox + 2 * kx : -(1 << 30); // out-of-range marker
+        ky0[m] = oy + 2 * ky;
+    }
+    long long cpo[9]; // coefficient plane offsets d * n (variable operators)
+#pragma unroll
+    for (int d = 0; d < 9; ++d) cpo[d] = (long long)d * n;
 #pragma unroll 1
     for (int q = 0; q < P; ++q) {
         const int pc = q & 3;
@@ -138,18 +176,19 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         const int g = P - 1 - q;
         const int lox = max(tx0 - g, 0), hix = min(tx0 + TX + g, nx);
         const int loy = max(ty0 - g, 0), hiy = min(ty0 + TY + g, nx);
-        const int gx0 = lox + ((lox & 1) ^ cx);
-        const int gy0 = loy + ((loy & 1) ^ cy);
-        for (int gy = gy0 + 2 * ty; gy < hiy; gy += 16) {
-            for (int gx = gx0 + 2 * tx; gx < hix; gx += 64) {
-                const int l = (gy - oy) * RX + (gx - ox);
-                const long long gi = (long long)gy * nx + gx;
+        const int lc = cy * RX + cx;
+#pragma unroll
+        for (int m = 0; m < KT; ++m) {
+            const int gx = kx0[m] + cx, gy = ky0[m] + cy;
+            if (gx >= lox && gx < hix && gy >= loy && gy < hiy) {
+                const int l = kl[m] + lc;
+                const double* cp = VAR ? A.coef + ((long long)gy * nx + gx) : nullptr;
                 double s = bs[l];
 #pragma unroll
                 for (int d = 0; d < 9; ++d) {
                     if (d == 4) continue;
                     const double a = S::CS ? cs[(d < 4 ? d : d - 1) * R + l]
-                                           : (VAR ? __ldg(A.coef + d * n + gi) : A.c[d]);
+                                           : (VAR ? __ldg(cp + cpo[d]) : A.c[d]);
                     s -= a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
                 }
                 xs[l] = s * iv[l];

@@ -11,6 +11,8 @@ import re
 ap = argparse.ArgumentParser()
 ap.add_argument("csv")
 ap.add_argument("--tail", type=int, default=0)
+ap.add_argument("--from-last", default=None,
+                help="summarise from the last launch of this kernel (e.g. k_cheb_init)")
 a = ap.parse_args()
 rows = []
 with open(a.csv) as f:
@@ -22,6 +24,10 @@ for d in csv.DictReader(lines):
     rows.append((name, float(d["Metric Value"]) * (1e-3 if d["Metric Unit"] == "ns" else 1.0)))
 if a.tail:
     rows = rows[-a.tail:]
+if a.from_last:
+    starts = [i for i, (n, _) in enumerate(rows) if n.startswith(a.from_last)]
+    if starts:
+        rows = rows[starts[-1]:]
 agg = collections.defaultdict(lambda: [0, 0.0])
 for n, us in rows:
     agg[n][0] += 1

@@ -1,0 +1,35 @@
+"""Workload for ncu launch lists of ONE KKT + preconditioner apply at a
+BASELINE config: one Newton step to set the preconditioner up, then
+oc_time_applies (warm-ups + `reps` timed applies).
+
+    python tools/profile_apply.py C4 [reps=1]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1806_05896_b200 import configs, optcon as oc  # noqa: E402
+
+KIND = {"gmres-pt": "pt", "minres-pd": "pd", "gmres-ppi": "ppi"}
+name = sys.argv[1] if len(sys.argv) > 1 else "C4"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+c = configs.ALL[name]
+kw = dict(pde=c.pde, alpha=c.alpha, beta=c.beta, y_d=c.y_d(), u_a=c.u_a, u_b=c.u_b)
+if c.pde == "convdiff":
+    kw["eps"] = c.eps
+if c.pde == "heat":
+    kw["tau"] = c.tau
+if c.y_a is not None:
+    kw.update(y_a=c.y_a, y_b=c.y_b)
+if c.obs is not None:
+    kw["observation"] = c.obs
+ctx = oc.Context(0)
+qp = oc.QpProblem(oc.ControlProblem(**kw), oc.Grid(c.level), ctx)
+try:
+    oc.ipm_solve(qp, oc.IpmParams(sigma=c.sigma, solver=c.solver, max_iterations=1,
+                                  gmres_restart=c.gmres_restart))
+except Exception as e:  # one IPM iteration does not converge: expected
+    print("solve:", type(e).__name__, e)
+print("MARK apply start", flush=True)
+k, p = qp.time_applies(KIND[c.solver], reps)
+print(f"{name}: kkt {k:.4f} ms, precond {p:.3f} ms")
