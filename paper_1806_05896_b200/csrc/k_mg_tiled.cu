@@ -75,9 +75,10 @@ struct SweepShape {
     static constexpr int H = 4 * NS;
     static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
     static constexpr int R = RX * RY;
-    // variable coefficients are staged for single sweeps; fused sweeps read
-    // them through L1 (the region grows with NS, the coefficient planes would not fit)
-    static constexpr bool CS = VAR && NS == 1;
+    // variable coefficients are staged in shared memory whenever the 11 planes
+    // fit (coalesced row copies, read once per launch for all fused sweeps);
+    // otherwise read through L1 (colour-strided, L2-bandwidth bound)
+    static constexpr bool CS = VAR && (size_t)11 * R * sizeof(double) <= 100 * 1024; // >= 2 CTAs/SM
     static constexpr int PLANES = CS ? 11 : 3; // x, b, inv (+ 8 off-diagonals)
     static constexpr size_t smem = (size_t)PLANES * R * sizeof(double);
 };
