@@ -15,6 +15,7 @@ rank (SURVEY §8e "replicas only"), scaling "weak", time = max over ranks.
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -209,6 +210,23 @@ def measured_peak_hbm():
 
 
 # ------------------------------------------------------------------ ours
+def measured_traffic(level, fuse):
+    """DRAM bytes per launch of the roofline kernel from a committed ncu capture
+    (profiles/*/roofline_traffic.json), or None."""
+    import glob
+
+    best = None
+    for f in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                           "profiles", "*", "roofline_traffic.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        if d.get("level") == level and d.get("fuse") == fuse:
+            best = {"bytes": d["dram_bytes_per_launch"], "source": os.path.relpath(f)}
+    return best
+
+
 def run_ours(args):
     import torch
 
@@ -362,7 +380,12 @@ def run_ours(args):
             prof[k][1] += pr[k][1]
     peak, peak_src = measured_peak_hbm()
     sweep_ms, sweep_n = prof["sweep"]
-    sweep_bytes = bytes_model.sweep_bytes(ny)
+    fuse = C.c_int(0)
+    _lib.check(_lib.load().oc_get_tuning(b"sweep_fuse", C.byref(fuse)))
+    fuse = max(1, min(5, fuse.value))
+    # the sampled launch fuses `fuse` sweeps; the byte model counts 4V per sweep
+    sweep_bytes = fuse * bytes_model.sweep_bytes(ny)
+    traffic = measured_traffic(args.level, fuse)
     achieved = sweep_bytes / (sweep_ms / sweep_n / 1e3) / 1e9 if sweep_n else None
     kkt_b, prec_b = bytes_model.apply_bytes("pt" if args.solver == "gmres-pt" else "pd",
                                             args.level, ny)
@@ -390,15 +413,19 @@ def run_ours(args):
             "data": "synthetic (seeded sine-mode y_d; no dataset exists for this path)",
             "config": workload(args.level, args.solver),
             "roofline": {
-                "bound": "hbm", "kernel": "k_gs_sweep (fine-level 4-colour GS sweep)",
+                "bound": "hbm",
+                "kernel": f"k_sweep (fine-level 4-colour GS, {fuse} fused sweeps per launch)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": traffic["bytes"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None,
                 "peak_source": peak_src,
                 "bytes_per_launch": sweep_bytes,
                 "avg_launch_ms": sweep_ms / sweep_n if sweep_n else None,
                 "launches_in_pass": sweep_n,
                 "note": "per-launch CUDA events on the solver stream, cells run one at a time; "
-                        "level-9 fields (2 MiB) are L2-resident between sweeps, see profiles/",
+                        "level-9 fields (2 MiB) are L2-resident between sweeps; traffic = DRAM "
+                        "read+write of the same launch from ncu (cold cache), see profiles/",
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

@@ -199,9 +199,10 @@ int oc_event_elapsed_between(oc_ctx* ctx_a, int slot_a, oc_ctx* ctx_b, int slot_
  * CTA 1: 32..63; 0 = not reached). out64 may be NULL. */
 int oc_debug_cluster_probes(int enable, unsigned long long* out64);
 /* Tuning knobs (process-wide): "sweep_tile" (-1 auto, 0: 64x32, 1: 32x32,
- * 2: 32x16, 3: 16x16 output tiles) and "sweep_fuse" (1 or 2 smoothing sweeps
- * per launch). Results are unchanged; only launch shapes differ. */
+ * 2: 32x16, 3: 16x16 output tiles) and "sweep_fuse" (1..5 smoothing sweeps
+ * per launch, default 2). Results are unchanged; only launch shapes differ. */
 int oc_set_tuning(const char* name, int value);
+int oc_get_tuning(const char* name, int* value);
 
 /* Q1 assembly into 9 coefficient arrays (fem.cpp:142-180; what: 0 mass,
  * 1 poisson, 2 convdiff(eps), 3 partial mass(obs), 4 lumped diagonal (n)). Host only. */

@@ -407,6 +407,18 @@ int oc_set_tuning(const char* name, int value)
     });
 }
 
+int oc_get_tuning(const char* name, int* value)
+{
+    return guarded([&] {
+        require(name, "oc_get_tuning");
+        require(value, "oc_get_tuning");
+        const std::string k = name;
+        if (k == "sweep_tile") *value = ocb::g_sweep_tile;
+        else if (k == "sweep_fuse") *value = ocb::g_sweep_fuse;
+        else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);
+    });
+}
+
 int oc_debug_cluster_probes(int enable, unsigned long long* out64)
 {
     return guarded([&] { ocb::cluster_probes(enable, out64); });

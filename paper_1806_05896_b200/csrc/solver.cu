@@ -333,7 +333,9 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
         ++s;
         double* out = outbuf(s);
         {
-            ProfScope ps(c, (k == 0 && ns == 1) ? kProfSweep : kProfCats);
+            // roofline sample: fine-level launches of the full fusion depth that
+            // read x and apply no prolongation (the steady-state launch)
+            ProfScope ps(c, (k == 0 && ns == F && cur != nullptr) ? kProfSweep : kProfCats);
             launch_sweep_tiled(c.stream, A, b, inv_at(k, bt), cur, out, true, cur == nullptr,
                                nullptr, ns);
         }
@@ -358,7 +360,7 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
         double* out = outbuf(s);
         {
             // the first post launch also applies the prolongation (fused)
-            ProfScope ps(c, (k == 0 && done > 0 && ns == 1) ? kProfSweep : kProfCats);
+            ProfScope ps(c, (k == 0 && done > 0 && ns == F) ? kProfSweep : kProfCats);
             launch_sweep_tiled(c.stream, A, b, inv_at(k, bt), cur, out, false, false,
                                done == 0 ? ec : nullptr, ns);
         }

@@ -10,15 +10,21 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-from paper_1806_05896_b200 import configs, optcon as oc  # noqa: E402
+from paper_1806_05896_b200 import _lib, configs, optcon as oc  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--level", type=int, default=9)
 ap.add_argument("--solver", default="gmres-pt")
 ap.add_argument("--cell", type=int, default=4)
 ap.add_argument("--repeat", type=int, default=2)
+ap.add_argument("--tile", type=int, default=None, help="sweep_tile knob (bench under concurrency: 0)")
+ap.add_argument("--fuse", type=int, default=None)
 a = ap.parse_args()
 
+if a.tile is not None:
+    _lib.check(_lib.load().oc_set_tuning(b"sweep_tile", a.tile))
+if a.fuse is not None:
+    _lib.check(_lib.load().oc_set_tuning(b"sweep_fuse", a.fuse))
 c = configs.C2_CELLS[a.cell].with_level(a.level, solver=a.solver)
 ctx = oc.Context(0)
 qp = oc.build_qp(oc.ControlProblem(alpha=c.alpha, beta=c.beta, y_d=c.y_d(), u_a=c.u_a, u_b=c.u_b),
