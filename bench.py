@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--sweep-fuse", type=int, default=None,
                     help="smoothing sweeps fused per tiled launch (1..5; library default if unset)")
     ap.add_argument("--sweep-tile", type=int, default=None, help="tiled sweep shape id (tuning)")
+    ap.add_argument("--cluster-bottom", type=int, default=None,
+                    help="1: levels <= 7 in the 16-CTA cluster kernel (default), 0: tiled + single CTA")
     return ap.parse_args()
 
 
@@ -124,8 +126,10 @@ def cpu_reference_sample(level, solver, ipm_iters=2, threads=None):
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    from paper_1806_05896_b200 import replicas
+
+    rank, _, _ = replicas.env_rank()
+    if not replicas.reference_runs_on(rank):
         return
     try:
         for _ in range(args.warmup):
@@ -230,12 +234,14 @@ def measured_traffic(level, fuse):
 def run_ours(args):
     import torch
 
-    from paper_1806_05896_b200 import _lib, bytes_model, optcon as oc
+    from paper_1806_05896_b200 import _lib, bytes_model, optcon as oc, replicas
 
     if args.sweep_fuse is not None:
         _lib.check(_lib.load().oc_set_tuning(b"sweep_fuse", int(args.sweep_fuse)))
     if args.sweep_tile is not None:
         _lib.check(_lib.load().oc_set_tuning(b"sweep_tile", int(args.sweep_tile)))
+    if args.cluster_bottom is not None:
+        _lib.check(_lib.load().oc_set_tuning(b"cluster_bottom", int(args.cluster_bottom)))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -319,14 +325,8 @@ def run_ours(args):
             iters += it
     launches = oc.Context.launch_count() - l0
     total_ms = sum(times)
-    t = torch.tensor([total_ms, float(iters)], dtype=torch.float64, device="cuda")
-    if dist:
-        tmax = t.clone()
-        dist.all_reduce(tmax[0:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tmax[1:2], op=dist.ReduceOp.SUM)
-        t = tmax
-    max_ms, all_iters = float(t[0]), float(t[1])
-    value = all_iters / (max_ms / 1e3)
+    max_ms, all_iters = replicas.reduce_step_stats(total_ms, iters, dist, device="cuda")
+    value = replicas.aggregate_rate(max_ms, all_iters)
 
     # ------------------------------------------- e2e through the C ABI (host buffers)
     pinned = [dict(y_d=torch.from_numpy(c.y_d()).pin_memory(),
@@ -359,12 +359,8 @@ def run_ours(args):
             e2e_it += sum(r[0] for r in res)
             h2d = sum(r[1] for r in res)
     d2h = sum(8 * (a.size) for a in host_out[0].values()) * len(cs)
-    e2e_value = e2e_it / (sum(e2e_ms) / 1e3)
-    if dist:
-        tt = torch.tensor([sum(e2e_ms), float(e2e_it)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt[0:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:2], op=dist.ReduceOp.SUM)
-        e2e_value = float(tt[1]) / (float(tt[0]) / 1e3)
+    e2e_max_ms, e2e_all_it = replicas.reduce_step_stats(sum(e2e_ms), e2e_it, dist, device="cuda")
+    e2e_value = replicas.aggregate_rate(e2e_max_ms, e2e_all_it)
 
     # ---- in-situ kernel timing pass (untimed; cells one at a time, events per launch)
     prof = {"sweep": [0.0, 0], "kkt": [0.0, 0], "prec": [0.0, 0]}

@@ -403,6 +403,7 @@ int oc_set_tuning(const char* name, int value)
         const std::string k = name;
         if (k == "sweep_tile") ocb::g_sweep_tile = value;
         else if (k == "sweep_fuse") ocb::g_sweep_fuse = value;
+        else if (k == "cluster_bottom") ocb::g_cluster_bottom = value;
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
     });
 }
@@ -415,6 +416,7 @@ int oc_get_tuning(const char* name, int* value)
         const std::string k = name;
         if (k == "sweep_tile") *value = ocb::g_sweep_tile;
         else if (k == "sweep_fuse") *value = ocb::g_sweep_fuse;
+        else if (k == "cluster_bottom") *value = ocb::g_cluster_bottom;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);
     });
 }

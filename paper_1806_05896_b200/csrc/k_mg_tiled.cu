@@ -355,6 +355,7 @@ void sweep_tile(int id, cudaStream_t s, const Op9& A, const double* b, const dou
 
 } // namespace
 
+int g_cluster_bottom = 1;
 int g_sweep_tile = -1; // tuning override: -1 auto, else tile id (see launch_sweep_tiled)
 int g_sweep_fuse = 2;  // sweeps fused per launch (measured best, profiles/r01/tuning.md)
 

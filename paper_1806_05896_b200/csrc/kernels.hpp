@@ -44,6 +44,7 @@ void launch_residual_restrict(cudaStream_t s, const Op9& A, const double* b, con
 // k_mg_tiled.cu: the same two operations, tiled for the large levels (>= 8):
 // `ns` fused sweeps per launch (1 or 2); g_sweep_tile overrides the tile choice.
 extern int g_sweep_tile;
+extern int g_cluster_bottom; // 1: levels <= 7 in the cluster kernel (default), 0: single-CTA bottom
 extern int g_sweep_fuse; // sweeps per launch in the V-cycle (1..5, temporal blocking)
 // inv = 1 / diag(A) precomputed per level (launch_inv_diag).
 void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,

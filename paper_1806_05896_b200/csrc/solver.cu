@@ -169,7 +169,7 @@ void Hierarchy::allocate(int level, int batch, int smoother)
     // is a slab level (>= 6); otherwise levels <= 6 in the single-CTA kernel
     // (the cluster kernel smooths with 4 colours; the lexicographic mode keeps
     // levels <= 6 in the single-CTA kernel and sweeps the others as wavefronts)
-    cluster_ = !lex_ && level >= 6 && cluster_bottom_supported();
+    cluster_ = !lex_ && g_cluster_bottom && level >= 6 && cluster_bottom_supported();
     const int top = cluster_ ? kClusterTopLevel : kBottomTopLevel;
     kb_ = 0;
     while (level - kb_ > top) ++kb_;

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-template <int MODE, int NACT>
+template <int MODE, int NACT, int ACC = 1>
 __global__ void k_pass(double* out, long long* cyc, int passes)
 {
     __shared__ double x[4 * 17 * 17];
@@ -21,14 +21,15 @@ __global__ void k_pass(double* out, long long* cyc, int passes)
         const int c = p & 3;
         if (MODE != 2 && t < NACT) {
             const int me = c * 289 + 18 + q;
-            double s = bb[me];
+            double s = bb[me], s2 = 0.0;
 #pragma unroll
             for (int d = 0; d < 9; ++d) {
                 if (d == 4) continue;
                 const int off = ((c + d) & 3) * 289 + (d / 3) * 17 + (d % 3);
-                s -= cf[d * 272 + (me & 255)] * x[q + off];
+                if (ACC == 2 && d > 4) s2 += cf[d * 272 + (me & 255)] * x[q + off];
+                else s -= cf[d * 272 + (me & 255)] * x[q + off];
             }
-            x[me] = s * 0.25;
+            x[me] = (ACC == 2 ? s - s2 : s) * 0.25;
         }
         if (MODE != 1) __syncthreads();
     }
@@ -57,5 +58,8 @@ int main()
     run(k_pass<1, 256>, "no barrier, 256 active");
     run(k_pass<1, 16>, "no barrier, 16 active");
     run(k_pass<2, 256>, "barrier only");
+    run(k_pass<0, 256, 2>, "full pass, 256 active, 2 accumulators");
+    run(k_pass<0, 16, 2>, "full pass, 16 active, 2 accumulators");
+    run(k_pass<1, 16, 2>, "no barrier, 16 active, 2 accumulators");
     return 0;
 }
