@@ -1,6 +1,7 @@
-// Geometric multigrid kernels (sm_100a, FP64): colour Gauss-Seidel sweeps,
-// fused residual + restriction, prolongation, Galerkin RAP, coarse LU and the
-// single-CTA bottom solver.
+// Geometric multigrid kernels (sm_100a, FP64): prolongation, residual norms
+// and the divergence check, Galerkin RAP, coarse LU and the single-CTA bottom
+// solver (the tiled sweeps live in k_mg_tiled.cu, the cluster bottom in
+// k_mg_cluster.cu, the lexicographic wavefront in k_mg_lex.cu).
 //
 // Reference semantics (multigrid.cpp):
 //   bilinear_prolongation  :10-42   P (1D weights 1/2,1,1/2; Dirichlet dropped), R = P^T
@@ -8,10 +9,11 @@
 //   MgHierarchy::build     :75-109  Galerkin R A P down to level 2 (or rediscretised base)
 //   cycle                  :111-132 pre sweeps, restrict residual, recurse, prolong, post
 //   solve                  :141-157 cycles from x=0, throw if ||r|| > 10 ||r_prev||
-// The smoother is a 4-colour symmetric Gauss-Seidel (colour = (gx&1) + 2(gy&1),
+// Default smoother: 4-colour symmetric Gauss-Seidel (colour = (gx&1) + 2(gy&1),
 // forward 0..3 / backward 3..0), the GPU-parallel replacement for the
 // lexicographic sweep: it keeps the V-cycle SPD for
-// symmetric operators, which MINRES with P_D requires.
+// symmetric operators, which MINRES with P_D requires. The lexicographic sweep
+// itself is the faithful mode (OC_SMOOTHER_LEX).
 #include "kernels.hpp"
 #include "lex_gs.cuh"
 
@@ -49,139 +51,6 @@ __device__ __forceinline__ double diag_at(const Op9& A, long long i, long long n
     double a = A.coef ? A.coef[4 * n + i] : A.c[4];
     if (A.diag) a += A.diag[i];
     return a;
-}
-
-// ------------------------------------------------------------------ sweeps
-// Out-of-place: reads x_in (with halo), writes x_out on the tile. In-place
-// would race with neighbouring CTAs that read their halo from this tile.
-template <int TX, int TY, int NS>
-__global__ void __launch_bounds__(256) k_gs_sweep(Op9 A, const double* __restrict__ b,
-                                                  const double* __restrict__ x,
-                                                  double* __restrict__ xo,
-                                                  const double* __restrict__ ec, int forward,
-                                                  int zero_init)
-{
-    constexpr int H = 4 * NS;
-    constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
-    extern __shared__ double sm[];
-    double* xs = sm;
-    double* bs = xs + RX * RY;
-    double* as = bs + RX * RY;
-
-    const int nx = A.nx;
-    const long long n = (long long)nx * nx;
-    const int nxc = (nx - 1) / 2;
-    const int tx0 = blockIdx.x * TX, ty0 = blockIdx.y * TY;
-    const int ox = tx0 - H, oy = ty0 - H;
-
-    for (int t = threadIdx.x; t < RX * RY; t += blockDim.x) {
-        const int gx = ox + t % RX, gy = oy + t / RX;
-        double xv = 0.0, bv = 0.0, av = 1.0;
-        if (gx >= 0 && gx < nx && gy >= 0 && gy < nx) {
-            const long long i = (long long)gy * nx + gx;
-            xv = zero_init ? 0.0 : x[i];
-            if (ec) xv = xv + prolong_at(ec, nxc, gx, gy); // axpy(1.0, P ec, x)
-            bv = b[i];
-            av = diag_at(A, i, n);
-        }
-        xs[t] = xv;
-        bs[t] = bv;
-        as[t] = av;
-    }
-    __syncthreads();
-
-    constexpr int P = 4 * NS;
-    for (int q = 0; q < P; ++q) {
-        const int pcol = q & 3;
-        const int c = forward ? pcol : 3 - pcol;
-        const int cx = c & 1, cy = c >> 1;
-        const int grow = P - 1 - q;
-        const int lox = max(tx0 - grow, 0), hix = min(tx0 + TX + grow, nx);
-        const int loy = max(ty0 - grow, 0), hiy = min(ty0 + TY + grow, nx);
-        const int gx0 = lox + (((lox & 1) != cx) ? 1 : 0);
-        const int gy0 = loy + (((loy & 1) != cy) ? 1 : 0);
-        const int cntx = hix > gx0 ? (hix - gx0 + 1) / 2 : 0;
-        const int cnty = hiy > gy0 ? (hiy - gy0 + 1) / 2 : 0;
-        for (int idx = threadIdx.x; idx < cntx * cnty; idx += blockDim.x) {
-            const int gx = gx0 + 2 * (idx % cntx), gy = gy0 + 2 * (idx / cntx);
-            const int l = (gy - oy) * RX + (gx - ox);
-            const long long i = (long long)gy * nx + gx;
-            double s = bs[l];
-#pragma unroll
-            for (int d = 0; d < 9; ++d) {
-                if (d == 4) continue;
-                const double a = A.coef ? A.coef[d * n + i] : A.c[d];
-                s -= a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
-            }
-            xs[l] = s / as[l];
-        }
-        __syncthreads();
-    }
-
-    for (int t = threadIdx.x; t < TX * TY; t += blockDim.x) {
-        const int gx = tx0 + t % TX, gy = ty0 + t / TX;
-        if (gx < nx && gy < nx) xo[(long long)gy * nx + gx] = xs[(gy - oy) * RX + (gx - ox)];
-    }
-}
-
-template <int TX, int TY, int NS>
-void sweep_launch(cudaStream_t s, const Op9& A, const double* b, const double* x, double* xo,
-                  bool forward, bool zero_init, const double* ec)
-{
-    constexpr int H = 4 * NS;
-    constexpr size_t smem = 3ull * (TX + 2 * H) * (TY + 2 * H) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_gs_sweep<TX, TY, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr = true;
-    }
-    dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
-    note_launch();
-    k_gs_sweep<TX, TY, NS><<<grid, 256, smem, s>>>(A, b, x, xo, ec, forward ? 1 : 0,
-                                                  zero_init ? 1 : 0);
-}
-
-// --------------------------------------------------------- residual/restrict
-template <int CX, int CY>
-__global__ void __launch_bounds__(CX* CY) k_residual_restrict(Op9 A, const double* __restrict__ b,
-                                                              const double* __restrict__ x,
-                                                              double* __restrict__ bc,
-                                                              double* __restrict__ xc)
-{
-    constexpr int FX = 2 * CX + 1, FY = 2 * CY + 1;
-    __shared__ double rs[FY * FX];
-    const int nx = A.nx;
-    const long long n = (long long)nx * nx;
-    const int nxc = (nx - 1) / 2;
-    const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY;
-    const int fx0 = 2 * cx0, fy0 = 2 * cy0;
-    for (int t = threadIdx.x; t < FX * FY; t += blockDim.x) {
-        const int gx = fx0 + t % FX, gy = fy0 + t / FX;
-        double r = 0.0;
-        if (gx < nx && gy < nx) {
-            const long long i = (long long)gy * nx + gx;
-            // multigrid.cpp:120-121: r = A x; r = rhs - r
-            r = b[i] - op_apply_at(A, x, gx, gy);
-        }
-        rs[t] = r;
-    }
-    __syncthreads();
-    const int cx = cx0 + threadIdx.x % CX, cy = cy0 + threadIdx.x / CX;
-    if (cx < nxc && cy < nxc) {
-        double s = 0.0;
-        // R row = P column: fine (2c..2c+2)^2 in ascending fine index order
-        for (int a = 0; a < 3; ++a) {
-            const double wy = (a == 1) ? 1.0 : 0.5;
-            for (int c = 0; c < 3; ++c) {
-                const double wx = (c == 1) ? 1.0 : 0.5;
-                s += (wx * wy) * rs[(2 * (cy - cy0) + a) * FX + 2 * (cx - cx0) + c];
-            }
-        }
-        const long long I = (long long)cy * nxc + cx;
-        bc[I] = s;
-        if (xc) xc[I] = 0.0; // coarse correction starts from 0 (multigrid.cpp:125)
-    }
 }
 
 __global__ void k_prolong_add(int nx, const double* __restrict__ ec, double* __restrict__ x)
@@ -626,31 +495,6 @@ __global__ void __launch_bounds__(LEX ? 64 : kBottomThreads)
 } // namespace
 
 // ------------------------------------------------------------- launchers
-void launch_gs_sweep(cudaStream_t s, const Op9& A, const double* b, const double* x, double* xo,
-                     bool forward, bool zero_init, const double* ec, int sweeps_fused)
-{
-    if (sweeps_fused == 2) {
-        if (A.nx >= 1000) sweep_launch<64, 32, 2>(s, A, b, x, xo, forward, zero_init, ec);
-        else if (A.nx >= 500) sweep_launch<32, 32, 2>(s, A, b, x, xo, forward, zero_init, ec);
-        else sweep_launch<32, 16, 2>(s, A, b, x, xo, forward, zero_init, ec);
-        return;
-    }
-    if (A.nx >= 1000) sweep_launch<64, 32, 1>(s, A, b, x, xo, forward, zero_init, ec);
-    else if (A.nx >= 500) sweep_launch<32, 32, 1>(s, A, b, x, xo, forward, zero_init, ec);
-    else if (A.nx >= 200) sweep_launch<32, 16, 1>(s, A, b, x, xo, forward, zero_init, ec);
-    else sweep_launch<16, 16, 1>(s, A, b, x, xo, forward, zero_init, ec);
-}
-
-void launch_residual_restrict(cudaStream_t s, const Op9& A, const double* b, const double* x,
-                              double* bc, double* xc)
-{
-    constexpr int CX = 32, CY = 8;
-    const int nxc = (A.nx - 1) / 2;
-    dim3 grid((nxc + CX - 1) / CX, (nxc + CY - 1) / CY);
-    note_launch();
-    k_residual_restrict<CX, CY><<<grid, CX * CY, 0, s>>>(A, b, x, bc, xc);
-}
-
 void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x)
 {
     const long long n = (long long)nx * nx;

@@ -30,19 +30,9 @@ struct BottomArgs {
     const int* perm;
 };
 
-// One symmetric-colour Gauss-Seidel sweep (4 colour passes fused via halo
-// recomputation), out of place: x_in -> x_out (must differ). forward: colours
-// 0..3, backward: 3..0. zero_init treats x_in as 0; if ec != nullptr,
-// x += P*ec (bilinear prolongation from the coarse level) is applied on load.
-void launch_gs_sweep(cudaStream_t s, const Op9& A, const double* b, const double* x_in,
-                     double* x_out, bool forward, bool zero_init, const double* ec,
-                     int sweeps_fused = 1);
-// bc = R (b - A x) with R = P^T, restricting to the coarse level (nxc = (nx-1)/2);
-// also zeroes the coarse iterate xc (if non-null).
-void launch_residual_restrict(cudaStream_t s, const Op9& A, const double* b, const double* x,
-                              double* bc, double* xc);
-// k_mg_tiled.cu: the same two operations, tiled for the large levels (>= 8):
-// `ns` fused sweeps per launch (1 or 2); g_sweep_tile overrides the tile choice.
+// k_mg_tiled.cu: the smoothing sweep and the fused residual + restriction
+// (bc = R (b - A x), R = P^T; also zeroes xc), tiled for the multi-CTA levels:
+// `ns` fused sweeps per launch (1..5); g_sweep_tile overrides the tile choice.
 extern int g_sweep_tile;
 extern int g_cluster_bottom; // 1: levels <= 7 in the cluster kernel (default), 0: single-CTA bottom
 extern int g_sweep_fuse; // sweeps per launch in the V-cycle (1..5, temporal blocking)
