@@ -24,25 +24,43 @@ namespace ocb {
 
 namespace {
 
+// P row of fine node (gx, gy): coarse parents in ascending column order,
+// branch-free (weight 0 = absent parent; no local-memory arrays)
 __device__ __forceinline__ double prolong_at(const double* __restrict__ ec, int nxc, int gx, int gy)
 {
-    // P row of fine node (gx, gy): coarse parents in ascending column order.
-    int px[2], py[2];
-    double wx[2], wy[2];
-    int cxn = 0, cyn = 0;
-    if (gx & 1) { px[0] = (gx - 1) >> 1; wx[0] = 1.0; cxn = 1; }
-    else {
-        if (gx / 2 - 1 >= 0) { px[cxn] = gx / 2 - 1; wx[cxn++] = 0.5; }
-        if (gx / 2 < nxc) { px[cxn] = gx / 2; wx[cxn++] = 0.5; }
+    int x0, x1, y0, y1;
+    double wx0, wx1, wy0, wy1;
+    if (gx & 1) {
+        x0 = x1 = (gx - 1) >> 1;
+        wx0 = 1.0;
+        wx1 = 0.0;
+    } else {
+        x0 = gx / 2 - 1;
+        x1 = gx / 2;
+        wx0 = x0 >= 0 ? 0.5 : 0.0;
+        wx1 = x1 < nxc ? 0.5 : 0.0;
     }
-    if (gy & 1) { py[0] = (gy - 1) >> 1; wy[0] = 1.0; cyn = 1; }
-    else {
-        if (gy / 2 - 1 >= 0) { py[cyn] = gy / 2 - 1; wy[cyn++] = 0.5; }
-        if (gy / 2 < nxc) { py[cyn] = gy / 2; wy[cyn++] = 0.5; }
+    if (gy & 1) {
+        y0 = y1 = (gy - 1) >> 1;
+        wy0 = 1.0;
+        wy1 = 0.0;
+    } else {
+        y0 = gy / 2 - 1;
+        y1 = gy / 2;
+        wy0 = y0 >= 0 ? 0.5 : 0.0;
+        wy1 = y1 < nxc ? 0.5 : 0.0;
     }
     double e = 0.0;
-    for (int a = 0; a < cyn; ++a)
-        for (int c = 0; c < cxn; ++c) e += (wx[c] * wy[a]) * ec[(long long)py[a] * nxc + px[c]];
+    if (wy0 != 0.0) {
+        const double* r = ec + (long long)y0 * nxc;
+        if (wx0 != 0.0) e += (wx0 * wy0) * r[x0];
+        if (wx1 != 0.0) e += (wx1 * wy0) * r[x1];
+    }
+    if (wy1 != 0.0) {
+        const double* r = ec + (long long)y1 * nxc;
+        if (wx0 != 0.0) e += (wx0 * wy1) * r[x0];
+        if (wx1 != 0.0) e += (wx1 * wy1) * r[x1];
+    }
     return e;
 }
 
