@@ -230,6 +230,57 @@ bool constant_stencil(const std::vector<double>& coef, int level, double c[9])
     return true;
 }
 
+void stencil9(int what, int level, double c[9])
+{
+    constexpr int L0 = 3;
+    const std::vector<double> a = what == 0 ? assemble_mass9(L0) : assemble_poisson9(L0);
+    const int nx = level_nx(L0);
+    const long long n = (long long)nx * nx, mid = (long long)(nx / 2) * nx + nx / 2;
+    double scale = 1.0;
+    if (what == 0)
+        for (int l = L0; l < level; ++l) scale *= 0.25; // exact: powers of two
+    for (int d = 0; d < 9; ++d) c[d] = what == 0 ? a[d * n + mid] * scale : a[d * n + mid];
+    if (what == 0 && level < L0) { // coarser than the reference grid: scale up
+        double up = 1.0;
+        for (int l = level; l < L0; ++l) up *= 4.0;
+        for (int d = 0; d < 9; ++d) c[d] = a[d * n + mid] * up;
+    }
+}
+
+std::vector<double> lumped_from_stencil(const double cM[9], int level)
+{
+    const int nx = level_nx(level);
+    std::vector<double> out((std::size_t)nx * nx, 0.0);
+    for (int gy = 0; gy < nx; ++gy)
+        for (int gx = 0; gx < nx; ++gx) {
+            double s = 0.0;
+            for (int d = 0; d < 9; ++d) {
+                const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
+                if (jx < 0 || jx >= nx || jy < 0 || jy >= nx) continue;
+                s += cM[d];
+            }
+            out[(std::size_t)gy * nx + gx] = s;
+        }
+    return out;
+}
+
+std::vector<double> apply_stencil(const double c[9], int level, const std::vector<double>& f)
+{
+    const int nx = level_nx(level);
+    std::vector<double> out((std::size_t)nx * nx, 0.0);
+    for (int gy = 0; gy < nx; ++gy)
+        for (int gx = 0; gx < nx; ++gx) {
+            double s = 0.0;
+            for (int d = 0; d < 9; ++d) {
+                const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
+                if (jx < 0 || jx >= nx || jy < 0 || jy >= nx) continue;
+                s += c[d] * f[(std::size_t)jy * nx + jx];
+            }
+            out[(std::size_t)gy * nx + gx] = s;
+        }
+    return out;
+}
+
 double supg_delta(int level, int ex, int ey, double eps)
 {
     const double h = 1.0 / double(1 << level);

@@ -34,6 +34,17 @@ std::vector<double> transpose9(const std::vector<double>& coef, int level);
 /// If every stored entry equals the interior stencil, return true and the
 /// 9 constants (the grid-constant operators L, M, M+tau L).
 bool constant_stencil(const std::vector<double>& coef, int level, double c[9]);
+/// The grid-constant stencils without assembling the level: the mass matrix
+/// scales exactly with h^2 (a power of 4) and the Q1 Poisson stiffness is
+/// h-independent in 2D, so the centre row of the level-3 assembly, scaled by
+/// 4^(3 - level), is bitwise the centre row of the full assembly
+/// (tests/test_assembly_shortcut.py). what: 0 mass, 1 Poisson.
+void stencil9(int what, int level, double c[9]);
+/// lumped_diag from the constant mass stencil: row sums over the in-domain
+/// neighbours in ascending column order (bitwise lumped_diag).
+std::vector<double> lumped_from_stencil(const double cM[9], int level);
+/// y = M f with the constant mass stencil, dropped boundary neighbours.
+std::vector<double> apply_stencil(const double c[9], int level, const std::vector<double>& f);
 /// Nodal interpolation of the default wind (fem.cpp:164-169) is inside
 /// assemble_convdiff9; this exposes the element-centre SUPG delta for tests.
 double supg_delta(int level, int ex, int ey, double eps);

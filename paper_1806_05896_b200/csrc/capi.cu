@@ -365,7 +365,8 @@ int oc_cheb_apply(oc_ctx* c, int level, double scale, const double* extra, int s
         ocb::Ctx& cx = c->ctx;
         const int nx = ocb::level_nx(level);
         const long long n = (long long)nx * nx;
-        const std::vector<double> M9 = ocb::assemble_mass9(level);
+        double cM[9];
+        ocb::stencil9(0, level, cM);
         ocb::ProbDev P{};
         P.nx = nx;
         P.ns = n;
@@ -375,7 +376,7 @@ int oc_cheb_apply(oc_ctx* c, int level, double scale, const double* extra, int s
         P.tau = scale;
         P.M.nx = nx;
         P.M.cscale = 1.0;
-        for (int d = 0; d < 9; ++d) P.M.c[d] = M9[d * n + n / 2];
+        for (int d = 0; d < 9; ++d) P.M.c[d] = cM[d];
         const double one = 1.0;
         ocb::DVec qw(1), bb((size_t)n), e, out((size_t)n), g((size_t)n), r0((size_t)n),
             r1((size_t)n), r2((size_t)n);

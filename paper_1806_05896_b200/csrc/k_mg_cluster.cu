@@ -262,7 +262,7 @@ struct C0Level {
 };
 
 template <bool FWD, int NX>
-__device__ void c0_sweep(const C0Level<NX>& L)
+__device__ __forceinline__ void c0_sweep(const C0Level<NX>& L)
 {
     using G = FullG<NX>;
     const int t = threadIdx.x;
@@ -288,7 +288,7 @@ __device__ void c0_sweep(const C0Level<NX>& L)
 }
 
 template <int NX>
-__device__ void c0_residual(const C0Level<NX>& L)
+__device__ __forceinline__ void c0_residual(const C0Level<NX>& L)
 {
     using G = FullG<NX>;
     for (int i = threadIdx.x; i < NX * NX; i += blockDim.x) {
@@ -373,23 +373,37 @@ __device__ void c0_load(const Op9& A, const C0Level<NX>& L)
     using G = FullG<NX>;
     const long long n = (long long)NX * NX;
     for (int i = threadIdx.x; i < G::S; i += blockDim.x) L.x[i] = 0.0; // padding stays zero
+    // off-diagonal planes: asynchronous global -> shared copies (all in flight;
+    // completed by cp.async.wait_all before the cluster barrier that ends loading)
     for (int i = threadIdx.x; i < NX * NX; i += blockDim.x) {
         const int gy = i / NX, gx = i - gy * NX;
         const int me = G::xi(gx, gy);
 #pragma unroll
         for (int d = 0; d < 9; ++d) {
-            const double v = op_entry(A, d, n, i);
-            L.coef[d * G::S + me] = v;
-            if (d == 4) L.inv[me] = 1.0 / v;
+            if (d == 4) continue;
+            if (A.coef) {
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(L.coef + d * G::S + me);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                             "l"(A.coef + d * n + i)
+                             : "memory");
+            } else {
+                L.coef[d * G::S + me] = A.c[d];
+            }
         }
+        const double v = op_entry(A, 4, n, i);
+        L.coef[4 * G::S + me] = v;
+        L.inv[me] = 1.0 / v;
     }
 }
 
 __device__ int g_probe_on = 0;
+// copy of g_probe_on taken once per launch: a global load per probe would stall
+// thread 0 (and through the next barrier, the CTA) even with probes disabled
+__shared__ int s_probe_on;
 __device__ unsigned long long g_tprobe[64];
 __device__ __forceinline__ void probe(unsigned rank, int i)
 {
-    if (threadIdx.x == 0 && rank < 2 && g_probe_on) {
+    if (threadIdx.x == 0 && rank < 2 && s_probe_on) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_tprobe[rank * 32 + i] = t;
@@ -527,6 +541,8 @@ __global__ void __launch_bounds__(kCT, 1)
     __shared__ double red[33];
     cg::cluster_group cl = cg::this_cluster();
     const int w = (int)cl.block_rank();
+    if (threadIdx.x == 0) s_probe_on = g_probe_on;
+    __syncthreads();
     probe(w, 0);
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Ly::BARS);
@@ -596,6 +612,7 @@ __global__ void __launch_bounds__(kCT, 1)
         C0Cycle<NC>::load(c0base, a, Ly::S1 ? 2 : 1);
         if (threadIdx.x < 81) lus[threadIdx.x] = a.lu[threadIdx.x];
         if (threadIdx.x < 9) perms[threadIdx.x] = a.perm[threadIdx.x];
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     }
     cl.sync();
     probe(w, 1);

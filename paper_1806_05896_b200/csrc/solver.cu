@@ -520,11 +520,10 @@ Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
     }
 
     // ---- operators (fem.cpp assembly restated in assembly.cpp)
-    const std::vector<double> M9 = assemble_mass9(level_);
+    // grid-constant stencils straight from the element formulas (no level-size
+    // assembly on the host; bitwise the centre rows of the full assembly)
     double cM[9];
-    if (!constant_stencil(M9, level_, cM) && nx_ >= 3)
-        throw RuntimeError("internal: mass stencil is not grid-constant");
-    if (nx_ < 3) for (int k = 0; k < 9; ++k) cM[k] = M9[k * ns_ + (ns_ / 2)];
+    stencil9(0, level_, cM);
     P = ProbDev{};
     P.nx = nx_;
     P.ns = ns_;
@@ -557,10 +556,8 @@ Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
             upload(baseT_[k], bt9.data(), bt9.size());
         }
     } else {
-        const std::vector<double> L9 = assemble_poisson9(level_);
         double cL[9];
-        if (!constant_stencil(L9, level_, cL))
-            for (int k = 0; k < 9; ++k) cL[k] = L9[k * ns_ + ns_ / 2];
+        stencil9(1, level_, cL);
         P.L = const_op(nx_, cL);
         P.LT = P.L;
         if (heat_) {
@@ -577,21 +574,11 @@ Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
     }
 
     // ---- problem vectors (build_qp qp.cpp:123-174, assemble_spacetime timedep.cpp:166-213)
-    const std::vector<double> ld = lumped_diag(level_);
+    const std::vector<double> ld = lumped_from_stencil(cM, level_);
     upload(ld_, ld.data(), ld.size());
-    std::vector<double> fn(ns_, 0.0);
-    if (d.f) fn = host_vec(d.f, ns_);
+    // f = M f_nodal (qp.cpp:150); zero unless a nodal source is given
     std::vector<double> mf(ns_, 0.0);
-    for (long long i = 0; i < ns_; ++i) {
-        const int gx = (int)(i % nx_), gy = (int)(i / nx_);
-        double s = 0.0;
-        for (int k = 0; k < 9; ++k) {
-            const int jx = gx + k % 3 - 1, jy = gy + k / 3 - 1;
-            if (jx < 0 || jx >= nx_ || jy < 0 || jy >= nx_) continue;
-            s += M9[k * ns_ + i] * fn[(long long)jy * nx_ + jx];
-        }
-        mf[i] = s;
-    }
+    if (d.f) mf = apply_stencil(cM, level_, host_vec(d.f, ns_));
     std::vector<double> fh(ny_);
     for (int k = 0; k < nt_; ++k)
         for (long long i = 0; i < ns_; ++i) fh[k * ns_ + i] = heat_ ? d.tau * mf[i] : mf[i];
