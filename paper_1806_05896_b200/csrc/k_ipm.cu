@@ -23,11 +23,11 @@ struct Loc {
 __device__ __forceinline__ Loc locate(const ProbDev& P, long long g)
 {
     Loc l;
-    l.k = (int)(g / P.ns);
+    l.k = ((int)g / (int)P.ns);
     l.off = (long long)l.k * P.ns;
     l.i = g - l.off;
-    l.gx = (int)(l.i % P.nx);
-    l.gy = (int)(l.i / P.nx);
+    l.gy = (int)l.i / P.nx;
+    l.gx = (int)l.i - l.gy * P.nx; // 32-bit: sizes < 2^31
     return l;
 }
 

@@ -76,7 +76,7 @@ __global__ void k_prolong_add(int nx, const double* __restrict__ ec, double* __r
     const long long n = (long long)nx * nx;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int gx = (int)(i % nx), gy = (int)(i / nx);
+    const int ii = (int)i, gy = ii / nx, gx = ii - gy * nx; // 32-bit: n < 2^31
     x[i] = x[i] + prolong_at(ec, (nx - 1) / 2, gx, gy);
 }
 
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kRedThreads) k_resid_norm_partials(Op9 A,
     double acc = 0.0;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        const int gx = (int)(i % nx), gy = (int)(i / nx);
+        const int ii = (int)i, gy = ii / nx, gx = ii - gy * nx; // 32-bit: n < 2^31
         const double r = b[i] - op_apply_at(A, x, gx, gy);
         acc += r * r;
     }

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kT) k_kkt_steady(ProbDev P, const double* __re
     double acc = 0.0;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        const int gx = (int)(i % nx), gy = (int)(i / nx);
+        const int ii = (int)i, gy = ii / nx, gx = ii - gy * nx; // 32-bit: n < 2^31
         const double My = op_apply_at(P.Mobs, y, gx, gy);
         const double Ltp = op_apply_at(P.LT, p, gx, gy);
         const double Mwv = stencil_diff(P.M, w, v, gx, gy);
@@ -111,9 +111,9 @@ __global__ void __launch_bounds__(kT) k_kkt_heat(ProbDev P, const double* __rest
     double acc = 0.0;
     for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < N;
          g += (long long)gridDim.x * blockDim.x) {
-        const int k = (int)(g / ns);
+        const int k = (int)g / (int)ns; // 32-bit: the space-time size is < 2^31
         const long long i = g - (long long)k * ns;
-        const int gx = (int)(i % nx), gy = (int)(i / nx);
+        const int ii = (int)i, gy = ii / nx, gx = ii - gy * nx; // 32-bit: n < 2^31
         const long long off = (long long)k * ns;
         const double sk = P.tau * P.qw[k];
         const double ak = P.alpha * P.tau * P.qw[k];
@@ -163,7 +163,7 @@ __global__ void k_cheb_init(ProbDev P, const double* __restrict__ b, const doubl
 {
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= P.ny) return;
-    const int k = (int)(g / P.ns);
+    const int k = ((int)g / (int)P.ns);
     g_out[g] = omega * cheb_invd(P, e, k, g) * b[g];
 }
 
@@ -174,9 +174,9 @@ __global__ void k_cheb_step(ProbDev P, const double* __restrict__ e, double omeg
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= P.ny) return;
     const long long ns = P.ns;
-    const int k = (int)(g / ns);
+    const int k = ((int)g / (int)ns);
     const long long i = g - (long long)k * ns;
-    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const int gy = (int)i / P.nx, gx = (int)i - gy * P.nx; // 32-bit
     double az = op_apply_at(P.M, cur + (long long)k * ns, gx, gy);
     if (P.heat) az = (P.tau * P.qw[k]) * az; // matvec: scale only when scale != 1
     if (e) az += e[g] * cur[g];
@@ -194,7 +194,7 @@ __global__ void k_control_2x2(ProbDev P, const double* __restrict__ tw,
 {
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= P.ny) return;
-    const int k = (int)(g / P.ns);
+    const int k = ((int)g / (int)P.ns);
     const double dM = P.M.c[4];
     const double sc = P.heat ? P.alpha * P.tau * P.qw[k] : P.alpha;
     const double a = sc * dM + tw[g];
@@ -216,7 +216,7 @@ __global__ void k_coupling_steady(ProbDev P, const double* __restrict__ vy,
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.ns) return;
-    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const int gy = (int)i / P.nx, gx = (int)i - gy * P.nx; // 32-bit
     const double Lvy = op_apply_at(P.L, vy, gx, gy);
     const double mw = op_apply_at(P.M, vw, gx, gy);
     const double mv = op_apply_at(P.M, vv, gx, gy);
@@ -230,10 +230,10 @@ __global__ void k_coupling_heat(ProbDev P, const double* __restrict__ vy,
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= P.ny) return;
     const long long ns = P.ns;
-    const int k = (int)(g / ns);
+    const int k = ((int)g / (int)ns);
     const long long i = g - (long long)k * ns;
     const long long off = (long long)k * ns;
-    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const int gy = (int)i / P.nx, gx = (int)i - gy * P.nx; // 32-bit
     double ly = op_apply_at(P.Mtl, vy + off, gx, gy);
     if (k > 0) ly -= op_apply_at(P.M, vy + off - ns, gx, gy);
     const double cz = P.tau * stencil_diff(P.M, vw + off, vv + off, gx, gy);
@@ -246,9 +246,9 @@ __global__ void k_schur_middle(ProbDev P, const double* __restrict__ ty,
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= P.ny) return;
     const long long ns = P.ns;
-    const int k = (int)(g / ns);
+    const int k = ((int)g / (int)ns);
     const long long i = g - (long long)k * ns;
-    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const int gy = (int)i / P.nx, gx = (int)i - gy * P.nx; // 32-bit
     const double tyv = ty ? ty[g] : 0.0;
     if (P.heat) {
         const double m = op_apply_at(P.M, t1 + (long long)k * ns, gx, gy);
@@ -265,7 +265,7 @@ __global__ void k_ppi_rhs1(ProbDev P, const double* __restrict__ vw, const doubl
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.ns) return;
-    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const int gy = (int)i / P.nx, gx = (int)i - gy * P.nx; // 32-bit
     rhs1[i] = stencil_diff(P.M, vw, vv, gx, gy) + rp[i];
 }
 
@@ -274,7 +274,7 @@ __global__ void k_ppi_t(ProbDev P, const double* __restrict__ ty, const double* 
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.ns) return;
-    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const int gy = (int)i / P.nx, gx = (int)i - gy * P.nx; // 32-bit
     const double tyv = ty ? ty[i] : 0.0;
     t[i] = op_apply_at(P.Mobs, v1, gx, gy) + (tyv * v1[i] - ry[i]);
 }
@@ -284,7 +284,8 @@ __global__ void k_op_apply(Op9 A, const double* __restrict__ x, double* __restri
     const long long n = (long long)A.nx * A.nx;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    y[i] = op_apply_at(A, x, (int)(i % A.nx), (int)(i / A.nx));
+    const int ii = (int)i, gy = ii / A.nx;
+    y[i] = op_apply_at(A, x, ii - gy * A.nx, gy);
 }
 
 __global__ void k_rhs_plus_mass(ProbDev P, const double* __restrict__ r,
@@ -292,7 +293,7 @@ __global__ void k_rhs_plus_mass(ProbDev P, const double* __restrict__ r,
 {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.ns) return;
-    const int gx = (int)(i % P.nx), gy = (int)(i / P.nx);
+    const int gy = (int)i / P.nx, gx = (int)i - gy * P.nx; // 32-bit
     rhs[i] = xnb ? r[i] + op_apply_at(P.M, xnb, gx, gy) : r[i];
 }
 
@@ -313,7 +314,7 @@ __global__ void k_mhat(ProbDev P, const double* __restrict__ ty, const double* _
     double br;
     double scale_d;
     if (P.heat) {
-        const int k = (int)(g / P.ns);
+        const int k = ((int)g / (int)P.ns);
         const double dc = P.qw[k] * d;
         br = P.tau * P.tau * d * d * s / (P.alpha * P.tau * dc * s + 1.0);
         scale_d = P.tau * dc;
