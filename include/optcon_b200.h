@@ -207,6 +207,9 @@ int oc_get_tuning(const char* name, int* value);
 /* Q1 assembly into 9 coefficient arrays (fem.cpp:142-180; what: 0 mass,
  * 1 poisson, 2 convdiff(eps), 3 partial mass(obs), 4 lumped diagonal (n)). Host only. */
 int oc_assemble9(int what, int level, double eps, const double* obs, double* coef);
+/* The same assembly on the device (what 0..3; coef host or device, 9 n). */
+int oc_assemble9_device(oc_ctx* ctx, int what, int level, double eps, const double* obs,
+                        double* coef);
 
 #ifdef __cplusplus
 }

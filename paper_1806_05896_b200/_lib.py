@@ -95,7 +95,7 @@ EXPORTS = [
     "oc_mg_solve", "oc_mg_depth", "oc_mg_level_matrix", "oc_mg_destroy", "oc_mg_smooth",
     "oc_cheb_apply", "oc_assemble9", "oc_launch_count", "oc_profile", "oc_profile_read",
     "oc_event_record", "oc_event_elapsed", "oc_debug_cluster_probes", "oc_event_elapsed_between",
-    "oc_set_tuning", "oc_get_tuning",
+    "oc_set_tuning", "oc_get_tuning", "oc_assemble9_device",
 ]
 
 _lib = None
@@ -142,6 +142,7 @@ def load():
     L.oc_mg_smooth.argtypes = [vp, vp, vp, C.c_int]
     L.oc_cheb_apply.argtypes = [vp, C.c_int, C.c_double, vp, C.c_int, vp, vp]
     L.oc_assemble9.argtypes = [C.c_int, C.c_int, C.c_double, vp, vp]
+    L.oc_assemble9_device.argtypes = [vp, C.c_int, C.c_int, C.c_double, vp, vp]
     L.oc_launch_count.restype = C.c_longlong
     L.oc_launch_count.argtypes = []
     L.oc_profile.argtypes = [vp, C.c_int]

@@ -503,4 +503,21 @@ int oc_assemble9(int what, int level, double eps, const double* obs, double* coe
     });
 }
 
+int oc_assemble9_device(oc_ctx* c, int what, int level, double eps, const double* obs, double* coef)
+{
+    return guarded([&] {
+        require(c, "oc_assemble9_device");
+        require(coef, "oc_assemble9_device");
+        if (level < 1 || level > 14) throw ocb::InvalidArgument("Grid: level out of range");
+        if (what < 0 || what > 3) throw ocb::InvalidArgument("oc_assemble9: unknown operator");
+        if (what == 2 && eps <= 0.0) throw ocb::InvalidArgument("assemble_convdiff: eps must be positive");
+        if (what == 3) require(obs, "oc_assemble9_device");
+        const size_t m = 9 * (size_t)ocb::level_n(level);
+        ocb::DVec d(m);
+        ocb::launch_assemble9(c->ctx.stream, what, level, eps, obs, d.get());
+        ocb::copy_any(c->ctx, coef, d.get(), m * sizeof(double));
+        c->ctx.sync();
+    });
+}
+
 } // extern "C"

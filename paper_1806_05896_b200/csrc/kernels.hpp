@@ -76,6 +76,14 @@ void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* 
                    bool forward, double* mbox, int* flags);
 double lex_sentinel_host();
 
+// k_assembly.cu: Q1 assembly on the device (what: 0 mass, 1 Poisson, 2 SUPG
+// convection-diffusion (eps), 3 partial-observation mass (obs = box, host
+// array of 4)) into 9 coefficient arrays; transpose9; out = 1*a + 1*b.
+void launch_assemble9(cudaStream_t s, int what, int level, double eps, const double* obs,
+                      double* coef);
+void launch_transpose9(cudaStream_t s, int nx, const double* in, double* out);
+void launch_add9(cudaStream_t s, long long m, const double* a, const double* b, double* out);
+
 // Cluster-resident bottom (k_mg_cluster.cu): levels <= 7 in one 16-CTA
 // thread-block cluster with distributed shared memory. ops[0] is the top
 // level handled (level 7 or 6).

@@ -537,23 +537,26 @@ Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
     P.M = const_op(nx_, cM);
     P.Mobs = P.M;
     if (convdiff_) {
-        const std::vector<double> L9 = assemble_convdiff9(level_, d.eps, true);
-        const std::vector<double> LT9 = transpose9(L9, level_);
-        upload(Lc_, L9.data(), L9.size());
-        upload(LTc_, LT9.data(), LT9.size());
+        // SUPG operator, its transpose and the per-level bases of the
+        // rediscretised hierarchies (qp.cpp:143-145), assembled on the device
+        Lc_.resize(9 * (size_t)ns_);
+        LTc_.resize(9 * (size_t)ns_);
+        launch_assemble9(ctx.stream, 2, level_, d.eps, nullptr, Lc_.get());
+        launch_transpose9(ctx.stream, nx_, Lc_.get(), LTc_.get());
         P.L = var_op(nx_, Lc_.get());
         P.LT = var_op(nx_, LTc_.get());
-        // per-level SUPG bases for the rediscretised hierarchies (qp.cpp:143-145)
         base_.clear();
         baseT_.clear();
         base_.resize(level_ - 1);
         baseT_.resize(level_ - 1);
         for (int k = 0; k + 2 <= level_; ++k) {
             const int l = level_ - k;
-            const std::vector<double> b9 = k == 0 ? L9 : assemble_convdiff9(l, d.eps, true);
-            const std::vector<double> bt9 = transpose9(b9, l);
-            upload(base_[k], b9.data(), b9.size());
-            upload(baseT_[k], bt9.data(), bt9.size());
+            const size_t m9 = 9 * (size_t)level_n(l);
+            base_[k].resize(m9);
+            baseT_[k].resize(m9);
+            if (k == 0) launch_copy(ctx.stream, Lc_.get(), base_[k].get(), (long long)m9);
+            else launch_assemble9(ctx.stream, 2, l, d.eps, nullptr, base_[k].get());
+            launch_transpose9(ctx.stream, level_nx(l), base_[k].get(), baseT_[k].get());
         }
     } else {
         double cL[9];
@@ -568,8 +571,8 @@ Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
         }
     }
     if (partial_obs_) {
-        const std::vector<double> Mo9 = assemble_partial_mass9(level_, d.obs);
-        upload(Mobsc_, Mo9.data(), Mo9.size());
+        Mobsc_.resize(9 * (size_t)ns_);
+        launch_assemble9(ctx.stream, 3, level_, 0.0, d.obs, Mobsc_.get());
         P.Mobs = var_op(nx_, Mobsc_.get());
     }
 
@@ -750,19 +753,22 @@ void Problem::setup_precond(int kind, const oc_ipm_params& p)
             HL_built_ = true;
         }
         if (!LTpMobs_) {
-            // left = L^T + M_obs (+ diag theta_y), sparse_add (precond.cpp:238)
-            std::vector<double> LT9 = convdiff_ ? transpose9(assemble_convdiff9(level_, eps_, true), level_)
-                                                : assemble_poisson9(level_);
-            std::vector<double> Mo9;
-            if (partial_obs_) {
-                Mo9.resize(9 * (size_t)ns_);
-                cuda_check(cudaMemcpy(Mo9.data(), Mobsc_.get(), Mo9.size() * sizeof(double),
-                                      cudaMemcpyDeviceToHost), "copy");
-            } else {
-                Mo9 = assemble_mass9(level_);
+            // left = L^T + M_obs (+ diag theta_y), sparse_add (precond.cpp:238), assembled
+            // on the device from the operators' 9 arrays
+            const size_t m9 = 9 * (size_t)ns_;
+            DVec lt, mo;
+            if (!convdiff_) {
+                lt.resize(m9);
+                launch_assemble9(ctx.stream, 1, level_, 0.0, nullptr, lt.get());
             }
-            for (size_t i = 0; i < LT9.size(); ++i) LT9[i] = 1.0 * LT9[i] + 1.0 * Mo9[i];
-            upload(LTpMobs_, LT9.data(), LT9.size());
+            if (!partial_obs_) {
+                mo.resize(m9);
+                launch_assemble9(ctx.stream, 0, level_, 0.0, nullptr, mo.get());
+            }
+            LTpMobs_.resize(m9);
+            launch_add9(ctx.stream, (long long)m9, convdiff_ ? LTc_.get() : lt.get(),
+                        partial_obs_ ? Mobsc_.get() : mo.get(), LTpMobs_.get());
+            ctx.sync(); // the temporaries return to the pool
         }
         Op9 left = var_op(nx_, LTpMobs_.get());
         left.diag = ty;

@@ -569,3 +569,19 @@ def assemble9(what: str, level: int, eps: float = 0.1, obs=None) -> np.ndarray:
     _lib.check(L.oc_assemble9(ASSEMBLE[what], level, C.c_double(eps),
                               C.c_void_p(o.ctypes.data), C.c_void_p(out.ctypes.data)))
     return out if what == "lumped" else out.reshape(9, n)
+
+
+def assemble9_device(what: str, level: int, eps: float = 0.1, obs=None,
+                     ctx: Optional[Context] = None) -> np.ndarray:
+    """The same assembly run on the device (k_assembly.cu); what: mass,
+    poisson, convdiff, partial_mass."""
+    ctx = ctx or default_context()
+    Grid(level)
+    if what not in ("mass", "poisson", "convdiff", "partial_mass"):
+        raise OptconInvalidArgument(f"assemble9_device: unsupported operator {what}")
+    n = ((1 << level) - 1) ** 2
+    out = np.zeros(9 * n)
+    o = np.ascontiguousarray(obs if obs is not None else [0.0, 1.0, 0.0, 1.0], dtype=np.float64)
+    _lib.check(ctx._L.oc_assemble9_device(ctx.h, ASSEMBLE[what], level, C.c_double(eps),
+                                          C.c_void_p(o.ctypes.data), C.c_void_p(out.ctypes.data)))
+    return out.reshape(9, n)

@@ -313,3 +313,19 @@ def test_convdiff_aggressive_sigma_nli(oc, ctx):
                                        u_a=-2.0, u_b=1.5), oc.Grid(level), ctx)
     r = oc.ipm_solve(qp, oc.IpmParams(sigma=0.4))
     assert r.stats.converged and r.stats.nli == 16
+
+
+# ------------------------------------------------------------ device assembly
+@pytest.mark.parametrize("what,kw", [("mass", {}), ("poisson", {}), ("convdiff", {"eps": 0.1}),
+                                     ("convdiff", {"eps": 0.02}),
+                                     ("partial_mass", {"obs": [0.0, 0.5, 0.0, 1.0]})])
+@pytest.mark.parametrize("ell", [3, 6, 9])
+def test_device_assembly_matches_host_assembly(oc, ctx, what, kw, ell):
+    # same element formulas, same accumulation order, no FMA contraction: equal
+    # to the host assembly up to the last ulp of hypot in the SUPG parameter
+    h = oc.assemble9(what, ell, **kw)
+    d = oc.assemble9_device(what, ell, ctx=ctx, **kw)
+    if what == "convdiff":
+        assert np.max(np.abs(d - h)) <= 4e-16 * np.max(np.abs(h))
+    else:
+        assert np.array_equal(d, h)
