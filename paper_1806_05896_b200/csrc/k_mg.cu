@@ -579,12 +579,13 @@ void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double*
                    int pre, int post, bool check, double* state, int* flags)
 {
     const size_t smem = bottom_smem_bytes(a);
-    static bool attr = false;
-    if (!attr) {
+    // thread-safe one-time setup (concurrent solves launch from several host threads)
+    static const bool attr = [] {
         cudaFuncSetAttribute(k_bottom<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(k_bottom<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     if (smem > 200 * 1024) throw std::runtime_error("bottom solver: level too large for one CTA");
     note_launch();
     if (a.lex)

@@ -316,12 +316,12 @@ void sweep_go(cudaStream_t s, const Op9& A, const double* b, const double* inv, 
               double* xo, bool forward, bool zero_init, const double* ec)
 {
     constexpr size_t smem = SweepShape<TX, TY, NS, VAR>::smem;
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] { // thread-safe one-time setup
         cudaFuncSetAttribute(k_sweep<TX, TY, NS, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
     note_launch();
     k_sweep<TX, TY, NS, VAR><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
@@ -355,9 +355,9 @@ void sweep_tile(int id, cudaStream_t s, const Op9& A, const double* b, const dou
 
 } // namespace
 
-int g_cluster_bottom = 1;
-int g_sweep_tile = -1; // tuning override: -1 auto, else tile id (see launch_sweep_tiled)
-int g_sweep_fuse = 2;  // sweeps fused per launch (measured best, profiles/r01/tuning.md)
+std::atomic<int> g_cluster_bottom{1};
+std::atomic<int> g_sweep_tile{-1}; // tuning override: -1 auto, else tile id (see launch_sweep_tiled)
+std::atomic<int> g_sweep_fuse{2};  // sweeps fused per launch (measured best, profiles/r01/tuning.md)
 
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
                      long long fds)
@@ -402,12 +402,12 @@ void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, 
     note_launch();
     if (A.coef) {
         constexpr size_t smem = (size_t)(XS + 10 * F) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
+        static const bool attr = [] { // thread-safe one-time setup
             cudaFuncSetAttribute(k_resid_restrict<CX, CY, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+            return true;
+        }();
+        (void)attr;
         k_resid_restrict<CX, CY, true><<<grid, 256, smem, s>>>(A, b, x, bc, xc);
     } else {
         constexpr size_t smem = (size_t)(XS + F) * sizeof(double);

@@ -4,6 +4,8 @@
 
 #include "oc_common.cuh"
 
+#include <atomic>
+
 namespace ocb {
 
 // Count of kernel launches issued by this library (bench "gpu_launches").
@@ -33,9 +35,10 @@ struct BottomArgs {
 // k_mg_tiled.cu: the smoothing sweep and the fused residual + restriction
 // (bc = R (b - A x), R = P^T; also zeroes xc), tiled for the multi-CTA levels:
 // `ns` fused sweeps per launch (1..5); g_sweep_tile overrides the tile choice.
-extern int g_sweep_tile;
-extern int g_cluster_bottom; // 1: levels <= 7 in the cluster kernel (default), 0: single-CTA bottom
-extern int g_sweep_fuse; // sweeps per launch in the V-cycle (1..5, temporal blocking)
+// process-wide tuning knobs (oc_set_tuning), read by every solving thread
+extern std::atomic<int> g_sweep_tile;
+extern std::atomic<int> g_cluster_bottom; // 1: levels <= 7 in the cluster kernel (default), 0: single-CTA bottom
+extern std::atomic<int> g_sweep_fuse;     // sweeps per launch in the V-cycle (1..5, temporal blocking)
 // inv = 1 / diag(A) precomputed per level (launch_inv_diag).
 void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                         const double* x, double* xo, bool forward, bool zero_init,

@@ -317,7 +317,8 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
     double* Abuf = xout;
     double* Bbuf = xb_[k].get();
     // sweeps are fused g_sweep_fuse at a time (same colour-pass sequence)
-    const int F = g_sweep_fuse < 1 ? 1 : (g_sweep_fuse > 5 ? 5 : g_sweep_fuse);
+    const int fz = g_sweep_fuse.load(std::memory_order_relaxed);
+    const int F = fz < 1 ? 1 : (fz > 5 ? 5 : fz);
     const int Lpre = (p.pre + F - 1) / F, Lpost = (p.post + F - 1) / F;
     const int S = Lpre + Lpost; // out-of-place launches; the last one must land in xout
     auto outbuf = [&](int s) { return ((S - s) % 2 == 0) ? Abuf : Bbuf; };
