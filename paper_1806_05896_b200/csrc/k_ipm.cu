@@ -429,6 +429,92 @@ void launch_objective(cudaStream_t s, const ProbDev& P, const IpmDev& S, double*
     k_objective_final<<<1, 32, 0, s>>>(part, P.heat, P.alpha, out);
 }
 
+// ---------------------------------------------------------- problem setup
+// split_bounds (qp.cpp:31-44) with the pinned-bound inflation (qp.cpp:162-166)
+// and the bound checks of ControlProblem::validate (qp.cpp:10-28), replicated
+// over the time blocks: za = [max(u_a,0); -min(u_b,0)], zb = [max(u_b,0); -min(u_a,0)].
+__global__ void k_split_bounds(long long ns, int nt, const double* __restrict__ ua,
+                               const double* __restrict__ ub, double* __restrict__ za,
+                               double* __restrict__ zb, int* flags)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    const double a = ua[i], b = ub[i];
+    if (a > 0.0 || b < 0.0) atomicOr(flags, kErrCtrlBounds);
+    double z[4] = {fmax(a, 0.0), -fmin(b, 0.0), fmax(b, 0.0), -fmin(a, 0.0)};
+    for (int h = 0; h < 2; ++h)
+        if (z[2 + h] - z[h] < 1e-12) z[2 + h] = z[h] + 1e-12;
+    const long long ny = ns * nt;
+    for (int k = 0; k < nt; ++k) {
+        const long long g = (long long)k * ns + i;
+        za[g] = z[0];
+        za[ny + g] = z[1];
+        zb[g] = z[2];
+        zb[ny + g] = z[3];
+    }
+}
+
+// state box check (y_a <= 0 <= y_b) of ControlProblem::validate
+__global__ void k_check_state_bounds(long long n, const double* __restrict__ ya,
+                                     const double* __restrict__ yb, int* flags)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && (ya[i] > 0.0 || yb[i] < 0.0)) atomicOr(flags, kErrStateBounds);
+}
+
+// row sums of the eliminated mass from its constant stencil (lumped_diag)
+__global__ void k_lumped(int nx, Op9 M, double* __restrict__ ld)
+{
+    const long long n = (long long)nx * nx;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int gy = (int)i / nx, gx = (int)i - gy * nx;
+    double s = 0.0;
+    for (int d = 0; d < 9; ++d) {
+        const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
+        if (jx < 0 || jx >= nx || jy < 0 || jy >= nx) continue;
+        s += M.c[d];
+    }
+    ld[i] = s;
+}
+
+// out[k ns + i] = scale * in[i] for every time block (or a plain copy per block)
+__global__ void k_replicate(long long ns, int nt, double scale, const double* __restrict__ in,
+                            double* __restrict__ out)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    const double v = scale * in[i];
+    for (int k = 0; k < nt; ++k) out[(long long)k * ns + i] = v;
+}
+
+void launch_split_bounds(cudaStream_t s, long long ns, int nt, const double* ua, const double* ub,
+                         double* za, double* zb, int* flags)
+{
+    note_launch();
+    k_split_bounds<<<blocks_for(ns), kT, 0, s>>>(ns, nt, ua, ub, za, zb, flags);
+}
+
+void launch_check_state_bounds(cudaStream_t s, long long n, const double* ya, const double* yb,
+                               int* flags)
+{
+    note_launch();
+    k_check_state_bounds<<<blocks_for(n), kT, 0, s>>>(n, ya, yb, flags);
+}
+
+void launch_lumped(cudaStream_t s, int nx, const Op9& M, double* ld)
+{
+    note_launch();
+    k_lumped<<<blocks_for((long long)nx * nx), kT, 0, s>>>(nx, M, ld);
+}
+
+void launch_replicate(cudaStream_t s, long long ns, int nt, double scale, const double* in,
+                      double* out)
+{
+    note_launch();
+    k_replicate<<<blocks_for(ns), kT, 0, s>>>(ns, nt, scale, in, out);
+}
+
 void launch_initial_point(cudaStream_t s, const ProbDev& P, const IpmDev& S)
 {
     note_launch();

@@ -253,6 +253,14 @@ void launch_objective(cudaStream_t s, const ProbDev& P, const IpmDev& S, double*
                       double* out);
 // initial_point (ipm.cpp:212-235)
 void launch_initial_point(cudaStream_t s, const ProbDev& P, const IpmDev& S);
+// problem setup on the device (build_qp qp.cpp:123-174 vectors)
+void launch_split_bounds(cudaStream_t s, long long ns, int nt, const double* ua, const double* ub,
+                         double* za, double* zb, int* flags);
+void launch_check_state_bounds(cudaStream_t s, long long n, const double* ya, const double* yb,
+                               int* flags);
+void launch_lumped(cudaStream_t s, int nx, const Op9& M, double* ld);
+void launch_replicate(cudaStream_t s, long long ns, int nt, double scale, const double* in,
+                      double* out);
 // u = w - v
 void launch_recover_control(cudaStream_t s, long long ny, const double* z, double* u);
 

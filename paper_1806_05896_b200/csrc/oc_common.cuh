@@ -123,6 +123,8 @@ enum ErrFlag : int {
     kErrThetaZ = 1 << 12,         // build_theta (ipm.cpp:44,56)
     kErrThetaY = 1 << 13,
     kErrLexStall = 1 << 14,       // lexicographic wavefront hand-off never arrived
+    kErrCtrlBounds = 1 << 15,     // ControlProblem::validate: u_a <= 0 <= u_b
+    kErrStateBounds = 1 << 16,    // ControlProblem::validate: y_a <= 0 <= y_b
 };
 
 } // namespace ocb

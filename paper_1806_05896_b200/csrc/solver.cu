@@ -468,24 +468,8 @@ Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
     has_sb_ = d.y_a != nullptr;
     partial_obs_ = d.has_obs != 0;
 
-    auto host_vec = [&](const double* p, size_t n) {
-        std::vector<double> v(n);
-        if (is_device_ptr(p)) cuda_check(cudaMemcpy(v.data(), p, n * sizeof(double), cudaMemcpyDeviceToHost), "copy");
-        else std::memcpy(v.data(), p, n * sizeof(double));
-        return v;
-    };
-    const std::vector<double> ua = host_vec(d.u_a, ns_), ub = host_vec(d.u_b, ns_);
-    for (long long i = 0; i < ns_; ++i)
-        if (ua[i] > 0.0 || ub[i] < 0.0)
-            throw InvalidArgument("ControlProblem: control bounds must satisfy u_a <= 0 <= u_b");
-    std::vector<double> yah, ybh;
-    if (has_sb_) {
-        yah = host_vec(d.y_a, ns_);
-        ybh = host_vec(d.y_b, ns_);
-        for (long long i = 0; i < ns_; ++i)
-            if (yah[i] > 0.0 || ybh[i] < 0.0)
-                throw InvalidArgument("ControlProblem: state bounds must satisfy y_a <= 0 <= y_b");
-    }
+    // (the bound checks of ControlProblem::validate run on the device with the
+    // bound splitting below)
     if (partial_obs_) {
         if (d.obs[0] > d.obs[1] || d.obs[2] > d.obs[3])
             throw InvalidArgument("ObservationRegion: empty box");
@@ -578,45 +562,53 @@ Problem::Problem(Ctx& c, const oc_problem_desc& d) : ctx(c)
     }
 
     // ---- problem vectors (build_qp qp.cpp:123-174, assemble_spacetime timedep.cpp:166-213)
-    const std::vector<double> ld = lumped_from_stencil(cM, level_);
-    upload(ld_, ld.data(), ld.size());
-    // f = M f_nodal (qp.cpp:150); zero unless a nodal source is given
-    std::vector<double> mf(ns_, 0.0);
-    if (d.f) mf = apply_stencil(cM, level_, host_vec(d.f, ns_));
-    std::vector<double> fh(ny_);
-    for (int k = 0; k < nt_; ++k)
-        for (long long i = 0; i < ns_; ++i) fh[k * ns_ + i] = heat_ ? d.tau * mf[i] : mf[i];
-    upload(f_, fh.data(), fh.size());
-    // split bounds (qp.cpp:31-44) with the pinned-bound inflation (qp.cpp:162-166)
-    std::vector<double> za(2 * ns_), zb(2 * ns_);
-    for (long long i = 0; i < ns_; ++i) {
-        if (ua[i] > ub[i]) throw InvalidArgument("split_bounds: u_a > u_b");
-        za[i] = std::max(ua[i], 0.0);
-        za[ns_ + i] = -std::min(ub[i], 0.0);
-        zb[i] = std::max(ub[i], 0.0);
-        zb[ns_ + i] = -std::min(ua[i], 0.0);
-    }
-    for (size_t i = 0; i < za.size(); ++i)
-        if (zb[i] - za[i] < 1e-12) zb[i] = za[i] + 1e-12;
-    std::vector<double> zah(2 * ny_), zbh(2 * ny_);
-    for (int k = 0; k < nt_; ++k)
-        for (long long i = 0; i < ns_; ++i) {
-            zah[k * ns_ + i] = za[i];
-            zah[ny_ + k * ns_ + i] = za[ns_ + i];
-            zbh[k * ns_ + i] = zb[i];
-            zbh[ny_ + k * ns_ + i] = zb[ns_ + i];
-        }
-    upload(za_, zah.data(), zah.size());
-    upload(zb_, zbh.data(), zbh.size());
+    // On the device from the caller's input arrays: only u_a, u_b, y_d (and
+    // y_a, y_b, f when given) cross the bus; the split bounds, lumped mass,
+    // f = M f_nodal and the time replication are computed here.
+    flags_.resize(1);
+    cuda_check(cudaMemsetAsync(flags_.get(), 0, sizeof(int), ctx.stream), "memset");
+    auto dev_in = [&](const double* src, size_t n, DVec& tmp) -> const double* {
+        if (is_device_ptr(src)) return src;
+        upload(tmp, src, n);
+        return tmp.get();
+    };
+    DVec t_ua, t_ub, t_f, t_yd;
+    const double* dua = dev_in(d.u_a, ns_, t_ua);
+    const double* dub = dev_in(d.u_b, ns_, t_ub);
+    za_.resize(2 * (size_t)ny_);
+    zb_.resize(2 * (size_t)ny_);
+    launch_split_bounds(ctx.stream, ns_, nt_, dua, dub, za_.get(), zb_.get(), flags_.get());
     if (has_sb_) {
-        upload(ya_, yah.data(), yah.size());
-        upload(yb_, ybh.data(), ybh.size());
+        upload(ya_, d.y_a, ns_);
+        upload(yb_, d.y_b, ns_);
+        launch_check_state_bounds(ctx.stream, ns_, ya_.get(), yb_.get(), flags_.get());
     }
-    {
-        std::vector<double> ydh(ny_);
-        const std::vector<double> src = host_vec(d.y_d, (size_t)d.y_d_len);
-        for (long long g = 0; g < ny_; ++g) ydh[g] = (d.y_d_len == ny_) ? src[g] : src[g % ns_];
-        upload(yd_, ydh.data(), ydh.size());
+    ld_.resize(ns_);
+    launch_lumped(ctx.stream, nx_, P.M, ld_.get());
+    f_.resize(ny_);
+    if (d.f) { // f = M f_nodal (qp.cpp:150), tau-scaled per time block for heat
+        DVec mf(ns_);
+        launch_op_apply(ctx.stream, P.M, dev_in(d.f, ns_, t_f), mf.get());
+        launch_replicate(ctx.stream, ns_, nt_, heat_ ? d.tau : 1.0, mf.get(), f_.get());
+        ctx.sync();
+    } else {
+        launch_fill(ctx.stream, f_.get(), 0.0, ny_);
+    }
+    if (d.y_d_len == ny_) {
+        upload(yd_, d.y_d, ny_);
+    } else {
+        yd_.resize(ny_);
+        launch_replicate(ctx.stream, ns_, nt_, 1.0, dev_in(d.y_d, ns_, t_yd), yd_.get());
+    }
+    {   // ControlProblem::validate bound checks (qp.cpp:10-28)
+        int fl = 0;
+        cuda_check(cudaMemcpyAsync(&fl, flags_.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream),
+                   "flags");
+        ctx.sync();
+        if (fl & kErrCtrlBounds)
+            throw InvalidArgument("ControlProblem: control bounds must satisfy u_a <= 0 <= u_b");
+        if (fl & kErrStateBounds)
+            throw InvalidArgument("ControlProblem: state bounds must satisfy y_a <= 0 <= y_b");
     }
     upload(qw_, qw.data(), qw.size());
     P.qw = qw_.get();
