@@ -211,25 +211,6 @@ std::vector<double> transpose9(const std::vector<double>& coef, int level)
     return t;
 }
 
-bool constant_stencil(const std::vector<double>& coef, int level, double c[9])
-{
-    const int nx = level_nx(level);
-    const long long n = (long long)nx * nx;
-    if (nx < 3) return false;
-    const long long mid = (long long)(nx / 2) * nx + nx / 2;
-    for (int d = 0; d < 9; ++d) c[d] = coef[d * n + mid];
-    for (int gy = 0; gy < nx; ++gy)
-        for (int gx = 0; gx < nx; ++gx) {
-            const long long i = (long long)gy * nx + gx;
-            for (int d = 0; d < 9; ++d) {
-                const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
-                if (jx < 0 || jx >= nx || jy < 0 || jy >= nx) continue;
-                if (coef[d * n + i] != c[d]) return false;
-            }
-        }
-    return true;
-}
-
 void stencil9(int what, int level, double c[9])
 {
     constexpr int L0 = 3;
@@ -279,12 +260,6 @@ std::vector<double> apply_stencil(const double c[9], int level, const std::vecto
             out[(std::size_t)gy * nx + gx] = s;
         }
     return out;
-}
-
-double supg_delta(int level, int ex, int ey, double eps)
-{
-    const double h = 1.0 / double(1 << level);
-    return delta_for(h, eps, ex * h, ey * h, true);
 }
 
 } // namespace ocb

@@ -31,9 +31,6 @@ std::vector<double> assemble_partial_mass9(int level, const double obs[4]);
 std::vector<double> lumped_diag(int level);
 /// Transpose of a 9-point operator: T(i, i+d) = A(i+d, i).
 std::vector<double> transpose9(const std::vector<double>& coef, int level);
-/// If every stored entry equals the interior stencil, return true and the
-/// 9 constants (the grid-constant operators L, M, M+tau L).
-bool constant_stencil(const std::vector<double>& coef, int level, double c[9]);
 /// The grid-constant stencils without assembling the level: the mass matrix
 /// scales exactly with h^2 (a power of 4) and the Q1 Poisson stiffness is
 /// h-independent in 2D, so the centre row of the level-3 assembly, scaled by
@@ -45,8 +42,5 @@ void stencil9(int what, int level, double c[9]);
 std::vector<double> lumped_from_stencil(const double cM[9], int level);
 /// y = M f with the constant mass stencil, dropped boundary neighbours.
 std::vector<double> apply_stencil(const double c[9], int level, const std::vector<double>& f);
-/// Nodal interpolation of the default wind (fem.cpp:164-169) is inside
-/// assemble_convdiff9; this exposes the element-centre SUPG delta for tests.
-double supg_delta(int level, int ex, int ey, double eps);
 
 } // namespace ocb
