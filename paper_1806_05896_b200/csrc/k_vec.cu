@@ -20,6 +20,8 @@ __global__ void __launch_bounds__(kRedThreads) k_dot_partials(const double* __re
 {
     __shared__ double sh[32];
     double acc = 0.0;
+    // unrolled so several loads are in flight; the accumulation order is unchanged
+#pragma unroll 4
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         acc += x[i] * y[i];
@@ -97,9 +99,43 @@ __global__ void k_mgs_step(const double* __restrict__ part, double* H, int ld, i
         w[k] += (-h) * vi[k];
 }
 
+// Modified Gram-Schmidt step i fused with the next dot product: h_ij = sum of
+// the kMgsBlocks partials part_in (fixed order), w -= h_ij v_i, and the
+// kMgsBlocks partials of <w, vnext> into part_out (one pass over w less than a
+// separate update + dot; a wider grid than kRedBlocks for memory parallelism).
+__global__ void __launch_bounds__(kRedThreads) k_mgs_dot(const double* __restrict__ part_in,
+                                                         double* H, int ld, int i, int j,
+                                                         const double* __restrict__ vi,
+                                                         double* __restrict__ w,
+                                                         const double* vnext,
+                                                         double* __restrict__ part_out, long long n)
+{
+    __shared__ double hs;
+    __shared__ double sh[32];
+    if (threadIdx.x < 32) {
+        const double s = sum_partials_warp(part_in, kMgsBlocks);
+        if (threadIdx.x == 0) {
+            hs = s;
+            if (blockIdx.x == 0) H[(long long)j * ld + i] = s;
+        }
+    }
+    __syncthreads();
+    const double h = hs;
+    double acc = 0.0;
+#pragma unroll 4
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long long)gridDim.x * blockDim.x) {
+        const double wn = w[k] + (-h) * vi[k];
+        w[k] = wn;
+        acc += wn * (vnext == w ? wn : vnext[k]);
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) part_out[blockIdx.x] = acc;
+}
+
 __global__ void k_gmres_givens(const double* __restrict__ part, GmresDev G, int j)
 {
-    const double s2 = sum_partials_warp(part, kRedBlocks);
+    const double s2 = sum_partials_warp(part, kMgsBlocks); // from the last k_mgs_dot
     if (threadIdx.x != 0) return;
     const double hnext = sqrt(s2);
     G.scal[1] = hnext;
@@ -285,6 +321,20 @@ void launch_mgs_step(cudaStream_t s, const double* part, const GmresDev& G, int 
 {
     note_launch();
     k_mgs_step<<<kRedBlocks * 4, kT, 0, s>>>(part, G.H, G.ld, i, j, vi, w, n);
+}
+
+void launch_mgs_dot(cudaStream_t s, const double* part_in, const GmresDev& G, int i, int j,
+                    const double* vi, double* w, const double* vnext, double* part_out, long long n)
+{
+    note_launch();
+    k_mgs_dot<<<kMgsBlocks, kRedThreads, 0, s>>>(part_in, G.H, G.ld, i, j, vi, w, vnext, part_out, n);
+}
+
+void launch_dot_partials_mgs(cudaStream_t s, const double* x, const double* y, long long n,
+                             double* part)
+{
+    note_launch();
+    k_dot_partials<<<kMgsBlocks, kRedThreads, 0, s>>>(x, y, n, part);
 }
 
 void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j)

@@ -203,6 +203,13 @@ struct GmresDev {
     int ld;
 };
 // h_i = <w, V_i> from partials, stored at H(i, j); then w -= h_i V_i
+// MGS step i + the next dot: w -= h_ij v_i (h_ij from part_in), part_out = partials
+// of <w, vnext> (vnext == w: ||w||^2), bit-identical to dot_partials after mgs_step
+// the first inner product of the orthogonalisation, on the kMgsBlocks grid
+void launch_dot_partials_mgs(cudaStream_t s, const double* x, const double* y, long long n,
+                             double* part);
+void launch_mgs_dot(cudaStream_t s, const double* part_in, const GmresDev& G, int i, int j,
+                    const double* vi, double* w, const double* vnext, double* part_out, long long n);
 void launch_mgs_step(cudaStream_t s, const double* part, const GmresDev& G, int i, int j,
                      const double* vi, double* w, long long n);
 // hnext from partials -> H(j+1, j), Givens update and back substitution for y (one thread)

@@ -1031,12 +1031,17 @@ oc_solve_report Problem::gmres(const oc_ipm_params& p, int kind, const double* b
                 launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(),
                            Z_[j].get(), kw_.get(), nullptr, nullptr);
             }
+            // modified Gram-Schmidt (krylov.cpp:150-157), each update fused with the
+            // next inner product; the last one yields ||w||^2
+            double* pa = part; // part_ holds 8 kRedBlocks = 2 kMgsBlocks partials
+            double* pb = part + kMgsBlocks;
+            launch_dot_partials_mgs(ctx.stream, kw_.get(), V_[0].get(), n, pa);
             for (int i = 0; i <= j; ++i) {
-                launch_dot_partials(ctx.stream, kw_.get(), V_[i].get(), n, part);
-                launch_mgs_step(ctx.stream, part, G, i, j, V_[i].get(), kw_.get(), n);
+                const double* next = i < j ? V_[i + 1].get() : kw_.get();
+                launch_mgs_dot(ctx.stream, pa, G, i, j, V_[i].get(), kw_.get(), next, pb, n);
+                std::swap(pa, pb);
             }
-            launch_dot_partials(ctx.stream, kw_.get(), kw_.get(), n, part);
-            launch_gmres_givens(ctx.stream, part, G, j);
+            launch_gmres_givens(ctx.stream, pa, G, j);
             launch_scale_inv(ctx.stream, kw_.get(), scal + 1, V_[j + 1].get(), n, stop_.get());
             launch_combine(ctx.stream, Ztab_.get(), yls_.get(), j + 1, x, n,
                            xbase ? kx2_.get() : nullptr);
