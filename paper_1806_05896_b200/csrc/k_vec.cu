@@ -70,7 +70,8 @@ __global__ void k_combine(const double* const* __restrict__ Z, const double* __r
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc = xb ? xb[i] : 0.0;
-    for (int k = 0; k < m; ++k) acc += y[k] * Z[k][i];
+#pragma unroll 4
+    for (int k = 0; k < m; ++k) acc += y[k] * Z[k][i]; // loads in flight, order unchanged
     x[i] = acc;
 }
 
