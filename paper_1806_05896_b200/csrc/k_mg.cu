@@ -80,10 +80,37 @@ __global__ void k_prolong_add(int nx, const double* __restrict__ ec, double* __r
     x[i] = x[i] + prolong_at(ec, (nx - 1) / 2, gx, gy);
 }
 
+// The block that completes last sums the partials (fixed order) and applies
+// the divergence check of MgHierarchy::solve (multigrid.cpp:141-157):
+// res = sqrt(sum); flag if res > 10 state[0] (unless init); state[0] = res.
+// Every block fences its partial before counting, the last one reads them
+// through L2; the counter is reset for the next launch.
+__device__ __forceinline__ void finish_norm_check(double* part, unsigned* counter, double* state,
+                                                  int* flags, int init)
+{
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x >= 32) return;
+    double v = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) v += __ldcg(part + i);
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+        const double res = sqrt(v);
+        if (!init && res > 10.0 * state[0]) atomicOr(flags, kErrMgDiverged);
+        state[0] = res;
+        *counter = 0u;
+    }
+}
+
 __global__ void __launch_bounds__(kRedThreads) k_resid_norm_partials(Op9 A,
                                                                      const double* __restrict__ b,
                                                                      const double* __restrict__ x,
-                                                                     double* __restrict__ part)
+                                                                     double* __restrict__ part,
+                                                                     unsigned* counter,
+                                                                     double* state, int* flags)
 {
     __shared__ double sh[32];
     const int nx = A.nx;
@@ -97,10 +124,12 @@ __global__ void __launch_bounds__(kRedThreads) k_resid_norm_partials(Op9 A,
     }
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
+    finish_norm_check(part, counter, state, flags, 0);
 }
 
 __global__ void __launch_bounds__(kRedThreads) k_sq_partials(const double* __restrict__ v,
-                                                             long long n, double* __restrict__ part)
+                                                             long long n, double* __restrict__ part,
+                                                             unsigned* counter, double* state)
 {
     __shared__ double sh[32];
     double acc = 0.0;
@@ -109,16 +138,7 @@ __global__ void __launch_bounds__(kRedThreads) k_sq_partials(const double* __res
         acc += v[i] * v[i];
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
-}
-
-__global__ void k_mg_check(const double* __restrict__ part, double* state, int* flags, int init)
-{
-    const double s = sum_partials_warp(part, kRedBlocks);
-    if (threadIdx.x == 0) {
-        const double res = sqrt(s);
-        if (!init && res > 10.0 * state[0]) atomicOr(flags, kErrMgDiverged);
-        state[0] = res;
-    }
+    finish_norm_check(part, counter, state, nullptr, 1);
 }
 
 // ----------------------------------------------------------------- Galerkin
@@ -520,25 +540,18 @@ void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x)
     k_prolong_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nx, ec, x);
 }
 
-void launch_residual_norm_partials(cudaStream_t s, const Op9& A, const double* b,
-                                   const double* x, double* part)
+void launch_residual_norm_check(cudaStream_t s, const Op9& A, const double* b, const double* x,
+                                double* part, unsigned* counter, double* state, int* flags)
 {
     note_launch();
-    k_resid_norm_partials<<<kRedBlocks, kRedThreads, 0, s>>>(A, b, x, part);
+    k_resid_norm_partials<<<kRedBlocks, kRedThreads, 0, s>>>(A, b, x, part, counter, state, flags);
 }
 
-void launch_mg_check(cudaStream_t s, const double* part, double* state, int* flags)
+void launch_norm_init(cudaStream_t s, const double* b, long long n, double* part,
+                      unsigned* counter, double* state)
 {
     note_launch();
-    k_mg_check<<<1, 32, 0, s>>>(part, state, flags, 0);
-}
-
-void launch_norm_init(cudaStream_t s, const double* b, long long n, double* part, double* state)
-{
-    note_launch();
-    k_sq_partials<<<kRedBlocks, kRedThreads, 0, s>>>(b, n, part);
-    note_launch();
-    k_mg_check<<<1, 32, 0, s>>>(part, state, nullptr, 1);
+    k_sq_partials<<<kRedBlocks, kRedThreads, 0, s>>>(b, n, part, counter, state);
 }
 
 void launch_rap(cudaStream_t s, const Op9& fine, double* coarse, const double* base,

@@ -49,14 +49,15 @@ void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, 
                                  double* bc, double* xc);
 // x += P ec
 void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x);
-// partial sums of |b - A x|^2 into part[kRedBlocks]
-void launch_residual_norm_partials(cudaStream_t s, const Op9& A, const double* b,
-                                   const double* x, double* part);
-// Divergence check of MgHierarchy::solve (multigrid.cpp:141-157):
-// res = sqrt(sum part); if (res > 10 * state[0]) flag; state[0] = res.
-void launch_mg_check(cudaStream_t s, const double* part, double* state, int* flags);
+// Divergence check of MgHierarchy::solve (multigrid.cpp:141-157) in one launch:
+// res = ||b - A x|| (kRedBlocks partials in part, summed in a fixed order by the
+// block that finishes last); flag if res > 10 state[0]; state[0] = res.
+// counter: one zero-initialised unsigned per hierarchy (reset by the kernel).
+void launch_residual_norm_check(cudaStream_t s, const Op9& A, const double* b, const double* x,
+                                double* part, unsigned* counter, double* state, int* flags);
 // state[0] = ||b||  (initial "previous residual")
-void launch_norm_init(cudaStream_t s, const double* b, long long n, double* part, double* state);
+void launch_norm_init(cudaStream_t s, const double* b, long long n, double* part,
+                      unsigned* counter, double* state);
 // Galerkin R A P into 9 coarse arrays; if base != nullptr the result is base + RAP.
 // batch > 1 (heat blocks): fine coef/diag and coarse arrays advance by the given strides.
 // If rem_out != nullptr the bare R A P is also written there (rediscretised chain).

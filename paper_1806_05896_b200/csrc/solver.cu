@@ -202,6 +202,9 @@ void Hierarchy::allocate(int level, int batch, int smoother)
     perm_.resize(9 * (size_t)batch);
     part_.resize(kRedBlocks);
     state_.resize(2);
+    cnt_.resize(1);
+    cuda_check(cudaMemsetAsync(cnt_.get(), 0, sizeof(unsigned), cudaStreamPerThread), "memset");
+    cuda_check(cudaStreamSynchronize(cudaStreamPerThread), "cudaStreamSynchronize");
     built_ = true;
 }
 
@@ -387,12 +390,11 @@ void Hierarchy::solve(Ctx& c, const double* b, double* x, const MgParams& p, int
         launch_fill(c.stream, x, 0.0, n);
         return;
     }
-    launch_norm_init(c.stream, b, n, part_.get(), state_.get());
+    launch_norm_init(c.stream, b, n, part_.get(), cnt_.get(), state_.get());
     const Op9 A = level_op(0, bt);
     for (int cyc = 0; cyc < p.cycles; ++cyc) {
         vcycle(c, 0, b, x, cyc == 0, p, bt, flags);
-        launch_residual_norm_partials(c.stream, A, b, x, part_.get());
-        launch_mg_check(c.stream, part_.get(), state_.get(), flags);
+        launch_residual_norm_check(c.stream, A, b, x, part_.get(), cnt_.get(), state_.get(), flags);
     }
     launch_check("multigrid solve");
 }

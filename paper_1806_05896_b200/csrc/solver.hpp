@@ -179,6 +179,7 @@ private:
     DVec lu_;
     DevArray<int> perm_;
     DVec part_, state_;
+    DevArray<unsigned> cnt_; // last-block counter of the fused divergence check
     bool built_ = false;
 };
 
