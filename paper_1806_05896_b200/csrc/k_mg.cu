@@ -540,18 +540,27 @@ void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x)
     k_prolong_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nx, ec, x);
 }
 
+// grid of the fused norm checks: one thread per node up to kNormBlocks blocks
+// (fixed per level, so the partial-sum order is deterministic)
+static unsigned norm_blocks(long long n)
+{
+    const long long b = (n + kRedThreads - 1) / kRedThreads;
+    return (unsigned)(b < 1 ? 1 : (b > kNormBlocks ? kNormBlocks : b));
+}
+
 void launch_residual_norm_check(cudaStream_t s, const Op9& A, const double* b, const double* x,
                                 double* part, unsigned* counter, double* state, int* flags)
 {
     note_launch();
-    k_resid_norm_partials<<<kRedBlocks, kRedThreads, 0, s>>>(A, b, x, part, counter, state, flags);
+    k_resid_norm_partials<<<norm_blocks((long long)A.nx * A.nx), kRedThreads, 0, s>>>(
+        A, b, x, part, counter, state, flags);
 }
 
 void launch_norm_init(cudaStream_t s, const double* b, long long n, double* part,
                       unsigned* counter, double* state)
 {
     note_launch();
-    k_sq_partials<<<kRedBlocks, kRedThreads, 0, s>>>(b, n, part, counter, state);
+    k_sq_partials<<<norm_blocks(n), kRedThreads, 0, s>>>(b, n, part, counter, state);
 }
 
 void launch_rap(cudaStream_t s, const Op9& fine, double* coarse, const double* base,

@@ -52,6 +52,7 @@ void launch_prolong_add(cudaStream_t s, int nx, const double* ec, double* x);
 // Divergence check of MgHierarchy::solve (multigrid.cpp:141-157) in one launch:
 // res = ||b - A x|| (kRedBlocks partials in part, summed in a fixed order by the
 // block that finishes last); flag if res > 10 state[0]; state[0] = res.
+// part: kNormBlocks doubles.
 // counter: one zero-initialised unsigned per hierarchy (reset by the kernel).
 void launch_residual_norm_check(cudaStream_t s, const Op9& A, const double* b, const double* x,
                                 double* part, unsigned* counter, double* state, int* flags);

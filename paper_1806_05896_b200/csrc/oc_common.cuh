@@ -26,6 +26,7 @@ struct Op9 {
 
 constexpr int kRedBlocks = 296;   // fixed reduction grid: 2 x 148 SMs (deterministic)
 constexpr int kMgsBlocks = 4 * kRedBlocks; // fixed grid of the GMRES orthogonalisation partials
+constexpr int kNormBlocks = 2048;           // max grid of the fused multigrid norm checks
 constexpr int kRedThreads = 256;
 
 __device__ __forceinline__ double op_coef(const Op9& A, int d, long long i, long long n)

@@ -200,7 +200,7 @@ void Hierarchy::allocate(int level, int batch, int smoother)
     }
     lu_.resize(81 * (size_t)batch);
     perm_.resize(9 * (size_t)batch);
-    part_.resize(kRedBlocks);
+    part_.resize(kNormBlocks);
     state_.resize(2);
     cnt_.resize(1);
     cuda_check(cudaMemsetAsync(cnt_.get(), 0, sizeof(unsigned), cudaStreamPerThread), "memset");
@@ -855,6 +855,8 @@ long long Problem::hierarchy_generation() const
            Hright_.generation() + Hheat_.generation();
 }
 
+constexpr long long kMaxGraphLaunches = 2000;
+
 void Problem::precond_apply(int kind, const double* r, double* out)
 {
     static const bool env_off = [] {
@@ -886,8 +888,13 @@ void Problem::precond_apply(int kind, const double* r, double* out)
         add_launches(g.launches);
         return;
     }
-    if (++g.uses < 2) { // first use runs directly (also performs one-time kernel setup)
+    if (++g.uses < 2 || g.launches > kMaxGraphLaunches) {
+        // first use runs directly (one-time kernel setup, and measures the
+        // apply's length); applies of thousands of launches (the heat time
+        // substitution) are not worth a graph instantiation
+        const long long l0 = t_launches;
         precond_apply_direct(kind, r, out);
+        if (g.uses == 1) g.launches = t_launches - l0;
         return;
     }
     const long long l0 = t_launches; // other threads launch concurrently: count our own
