@@ -15,7 +15,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_ref", "liboptcon_ref.so")
+# OPTCON_REF_LIB selects a rounding-variant build of the same sources (Makefile EXTRA)
+LIB_PATH = os.environ.get("OPTCON_REF_LIB") or os.path.join(_HERE, "_ref", "liboptcon_ref.so")
 
 _dp = C.POINTER(C.c_double)
 
