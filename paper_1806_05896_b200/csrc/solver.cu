@@ -128,6 +128,7 @@ Ctx::~Ctx()
     if (ev1) cudaEventDestroy(ev1);
     for (auto& e : user_ev)
         if (e) cudaEventDestroy(e);
+    for (auto& g : spare_graphs) cudaGraphExecDestroy(g.exec);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -842,10 +843,17 @@ Problem::~Problem()
     drop_graphs();
 }
 
+bool graph_reuse();
+
 void Problem::drop_graphs()
 {
-    for (auto& kv : graphs_)
-        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& kv : graphs_) {
+        if (!kv.second.exec) continue;
+        if (graph_reuse() && ctx.spare_graphs.size() < Ctx::kMaxSpareGraphs)
+            ctx.spare_graphs.push_back({kv.second.launches, kv.second.exec});
+        else
+            cudaGraphExecDestroy(kv.second.exec);
+    }
     graphs_.clear();
 }
 
@@ -856,6 +864,33 @@ long long Problem::hierarchy_generation() const
 }
 
 constexpr long long kMaxGraphLaunches = 2000;
+
+bool graph_reuse()
+{
+    static const bool on = [] {
+        const char* e = getenv("OC_GRAPH_REUSE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// A spare exec of the same length that accepts this graph (same topology and
+// kernels; only parameters may differ), or nullptr.
+static cudaGraphExec_t take_spare(Ctx& ctx, cudaGraph_t graph, long long launches)
+{
+    auto& sp = ctx.spare_graphs;
+    for (size_t i = sp.size(); i-- > 0;) {
+        if (sp[i].launches != launches) continue;
+        cudaGraphExecUpdateResultInfo info{};
+        if (cudaGraphExecUpdate(sp[i].exec, graph, &info) == cudaSuccess) {
+            cudaGraphExec_t e = sp[i].exec;
+            sp.erase(sp.begin() + (long)i);
+            return e;
+        }
+        cudaGetLastError(); // topology differs: try the next one
+    }
+    return nullptr;
+}
 
 void Problem::precond_apply(int kind, const double* r, double* out)
 {
@@ -910,8 +945,8 @@ void Problem::precond_apply(int kind, const double* r, double* out)
     }
     cuda_check(cudaStreamEndCapture(ctx.stream, &graph), "cudaStreamEndCapture");
     const long long captured = t_launches - l0;
-    cudaGraphExec_t exec = nullptr;
-    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphExec_t exec = graph_reuse() ? take_spare(ctx, graph, captured) : nullptr;
+    const cudaError_t e = exec ? cudaSuccess : cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     cuda_check(e, "cudaGraphInstantiate");
     g.exec = exec;

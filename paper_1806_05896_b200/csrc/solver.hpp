@@ -103,6 +103,15 @@ struct Ctx {
     double* hscal = nullptr; // pinned host mirror (64 doubles)
     int* hflags = nullptr;   // pinned host mirror (8 ints)
     Profiler prof;
+    // Instantiated preconditioner graphs released by closed problems, kept for
+    // the next problem on this context: a new capture of the same apply shape
+    // is patched into one with cudaGraphExecUpdate instead of instantiated.
+    struct SpareGraph {
+        long long launches;
+        cudaGraphExec_t exec;
+    };
+    std::vector<SpareGraph> spare_graphs;
+    static constexpr size_t kMaxSpareGraphs = 64;
     explicit Ctx(int dev);
     ~Ctx();
     void sync();
