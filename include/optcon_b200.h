@@ -198,6 +198,9 @@ int oc_event_elapsed_between(oc_ctx* ctx_a, int slot_a, oc_ctx* ctx_b, int slot_
  * multigrid bottom kernel and read the last launch's 64 stamps (CTA 0: 0..31,
  * CTA 1: 32..63; 0 = not reached). out64 may be NULL. */
 int oc_debug_cluster_probes(int enable, unsigned long long* out64);
+/* tuning aid: the dense 225 x 225 operator of the V-cycle below level 5 that the
+   cluster bottom applies (row-major, batch element 0) */
+int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
 /* Tuning knobs (process-wide): "sweep_tile" (-1 auto, 0: 64x32, 1: 32x32,
  * 2: 32x16, 3: 16x16 output tiles) and "sweep_fuse" (1..5 smoothing sweeps
  * per launch, default 2). Results are unchanged; only launch shapes differ. */

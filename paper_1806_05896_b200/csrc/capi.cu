@@ -405,6 +405,7 @@ int oc_set_tuning(const char* name, int value)
         if (k == "sweep_tile") ocb::g_sweep_tile = value;
         else if (k == "sweep_fuse") ocb::g_sweep_fuse = value;
         else if (k == "cluster_bottom") ocb::g_cluster_bottom = value;
+        else if (k == "cluster_top8") ocb::g_cluster_top8 = value;
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
     });
 }
@@ -418,7 +419,21 @@ int oc_get_tuning(const char* name, int* value)
         if (k == "sweep_tile") *value = ocb::g_sweep_tile;
         else if (k == "sweep_fuse") *value = ocb::g_sweep_fuse;
         else if (k == "cluster_bottom") *value = ocb::g_cluster_bottom;
+        else if (k == "cluster_top8") *value = ocb::g_cluster_top8;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);
+    });
+}
+
+int oc_debug_coarse_op(oc_mg* m, int pre, int post, double* out)
+{
+    return guarded([&] {
+        require(m, "oc_debug_coarse_op");
+        m->h.ensure_coarse_op(*m->ctx, pre, post);
+        const double* d = m->h.coarse_op();
+        if (!d) throw ocb::InvalidArgument("oc_debug_coarse_op: hierarchy has no cluster bottom");
+        ocb::copy_any(*m->ctx, out, d, (size_t)ocb::kCoarseOpN * ocb::kCoarseOpN * 8);
+        m->ctx->sync();
+        ocb::cuda_check(cudaGetLastError(), "coarse operator");
     });
 }
 

@@ -42,6 +42,8 @@ namespace {
 
 constexpr int kCS = 16;  // CTAs per cluster (non-portable size)
 constexpr int kCT = 256; // threads per CTA
+constexpr int kCopN = 225;   // level-4 nodes (15 x 15): dense V-cycle operator below level 5
+constexpr int kCopRows = 15; // rows of it per CTA 1..15
 
 // --------------------------------------------------- mbarrier / DSM primitives
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -92,9 +94,9 @@ __host__ __device__ constexpr int fl2(int v) { return (v - (((v % 2) + 2) % 2)) 
 // levels by one leading row) that stay zero, so a neighbour outside the
 // domain reads 0 and every neighbour of a thread's colour-c node is
 // x[q + nb(c, dx, dy)] with a compile-time offset and q = rr * SX + cc.
-template <int NX_, int RP_>
+template <int NX_, int RP_, int NPT_ = 1>
 struct SlabG {
-    static constexpr int NX = NX_, RP = RP_;
+    static constexpr int NX = NX_, RP = RP_, NPT = NPT_; // NPT node positions per colour per thread
     static constexpr int WX = (NX + 1) / 2;     // columns per colour row
     static constexpr int SX = WX + 1;           // padded row stride
     static constexpr int RH = RP / 2;           // colour rows per band
@@ -103,8 +105,8 @@ struct SlabG {
     static constexpr int GROUP = RH * WX;       // threads owning nodes (one per colour)
     static constexpr int RS = RP * NX;          // row-major residual of own rows
     static_assert(RP % 2 == 0, "even row bands keep the colour parity per CTA");
-    static_assert(GROUP <= kCT, "one node per colour per thread");
-    static_assert(2 * NX <= kCT, "one halo node per thread");
+    static_assert(GROUP <= NPT * kCT, "NPT nodes per colour per thread");
+    static_assert(NPT == 1 || GROUP == NPT * kCT, "multi-position levels fill every thread");
     // planar index of (gx, local row lr); lr = gy - r0 + 1 in [0, RP + 1]
     __host__ __device__ static constexpr int xi(int gx, int lr)
     {
@@ -154,6 +156,31 @@ struct Own {
     __device__ __forceinline__ bool valid(int c) const { return thr && gx(c) < G::NX && gy(c) < G::NX; }
     __device__ __forceinline__ int me(int c) const { return q + G::nb(c, 0, 0); }
     __device__ __forceinline__ int slot(int c) const { return c * G::GROUP + threadIdx.x; }
+};
+
+// The NPT nodes per colour of a thread on a multi-position slab level (the
+// level-8 top): position m is colour-sub-lattice index t + 256 m, so a warp
+// covers 32 consecutive columns of one colour row.
+template <class G>
+struct OwnM {
+    static constexpr int N = G::NPT;
+    int cc[N], rr[N], q[N];
+    int r0;
+    __device__ explicit OwnM(int w)
+    {
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+            const int g = threadIdx.x + kCT * m;
+            rr[m] = g / G::WX;
+            cc[m] = g - rr[m] * G::WX;
+            q[m] = rr[m] * G::SX + cc[m];
+        }
+        r0 = G::RP * w;
+    }
+    __device__ __forceinline__ int gx(int m, int c) const { return 2 * cc[m] + (c & 1); }
+    __device__ __forceinline__ int gy(int m, int c) const { return r0 + 2 * rr[m] + (c >> 1); }
+    __device__ __forceinline__ bool valid(int m, int c) const { return gx(m, c) < G::NX && gy(m, c) < G::NX; }
+    __device__ __forceinline__ int me(int m, int c) const { return q[m] + G::nb(c, 0, 0); }
 };
 
 // x(gx+dx, gy+dy) of the colour-c node from the local planar band (own rows +
@@ -221,6 +248,16 @@ struct Halo {
             st_async(mapa(xs + 8u * G::xi(o.gx(c), 0), (uint32_t)(w + 1)), v,
                      mapa(bar + 8 * c, (uint32_t)(w + 1)));
     }
+    // multi-position levels: the node at column gx of colour row rr
+    __device__ __forceinline__ void push_at(int gx, int rr, double v, int c) const
+    {
+        if (c < 2 && rr == 0 && has_up())
+            st_async(mapa(xs + 8u * G::xi(gx, G::RP + 1), (uint32_t)(w - 1)), v,
+                     mapa(bar + 8 * c, (uint32_t)(w - 1)));
+        if (c >= 2 && rr == G::RH - 1 && has_dn())
+            st_async(mapa(xs + 8u * G::xi(gx, 0), (uint32_t)(w + 1)), v,
+                     mapa(bar + 8 * c, (uint32_t)(w + 1)));
+    }
     __device__ __forceinline__ void passed(int c) { pend |= 1u << c; }
 };
 
@@ -247,6 +284,34 @@ __device__ __forceinline__ void slab_sweep(double* xs, Halo<G>& H, const Own<G>&
         }
         __syncthreads(); // CTA-local visibility; every halo read of this pass is done
         if (act) H.push(o, v, c);
+        H.passed(c);
+    }
+}
+
+// The same on a multi-position level: upd(m, c) for the thread's nodes m.
+template <bool FWD, class G, typename U>
+__device__ __forceinline__ void slab_sweep_m(double* xs, Halo<G>& H, const OwnM<G>& o, const U& upd)
+{
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int c = FWD ? p : 3 - p;
+        if (c < 2) {
+            H.ensure(2);
+            H.ensure(3);
+        } else {
+            H.ensure(0);
+            H.ensure(1);
+        }
+        double v[G::NPT];
+#pragma unroll
+        for (int m = 0; m < G::NPT; ++m) v[m] = o.valid(m, c) ? upd(m, c) : 0.0;
+#pragma unroll
+        for (int m = 0; m < G::NPT; ++m)
+            if (o.valid(m, c)) xs[o.me(m, c)] = v[m];
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < G::NPT; ++m)
+            if (o.valid(m, c)) H.push_at(o.gx(m, c), o.rr[m], v[m], c);
         H.passed(c);
     }
 }
@@ -415,14 +480,15 @@ template <int NX>
 struct C0Cycle {
     static constexpr int DEPTH = 1 + C0Cycle<NX / 2>::DEPTH;
     static constexpr size_t doubles() { return 13 * (size_t)FullG<NX>::S + C0Cycle<NX / 2>::doubles(); }
+    // x and b first: below the top CTA-0 level the cluster kernel keeps only them
     __device__ static void layout(double* base, C0Level<NX>& L)
     {
         constexpr int S = FullG<NX>::S;
-        L.coef = base;
-        L.x = base + 9 * S;
-        L.b = L.x + S;
-        L.inv = L.b + S;
-        L.r = L.inv + S;
+        L.x = base;
+        L.b = base + S;
+        L.inv = base + 2 * S;
+        L.r = base + 3 * S;
+        L.coef = base + 4 * S;
     }
     __device__ static void load(double* base, const BottomArgs& a, int k)
     {
@@ -431,16 +497,21 @@ struct C0Cycle {
         c0_load<NX>(a.ops[k], L);
         C0Cycle<NX / 2>::load(base + 13 * FullG<NX>::S, a, k + 1);
     }
-    __device__ __noinline__ static void run(double* base, const double* lu, const int* perm, int pre,
-                                            int post)
+    __device__ static void load_top(double* base, const BottomArgs& a, int k) // this level only
+    {
+        C0Level<NX> L;
+        layout(base, L);
+        c0_load<NX>(a.ops[k], L);
+    }
+    // pre-smoothing, residual and restriction into the next level's b (x zeroed)
+    __device__ static void run_pre(double* base, int pre)
     {
         constexpr int NC = NX / 2;
         constexpr int PB = 8 + 4 * (3 - DEPTH); // probe slots: level 31 -> 8.., 15 -> 12.., 7 -> 16..
         C0Level<NX> L;
         layout(base, L);
-        double* cbase = base + 13 * FullG<NX>::S;
         C0Level<NC> Lc;
-        C0Cycle<NC>::layout(cbase, Lc);
+        C0Cycle<NC>::layout(base + 13 * FullG<NX>::S, Lc);
         for (int s = 0; s < pre; ++s) c0_sweep<true, NX>(L);
         probe(0, PB);
         c0_residual<NX>(L);
@@ -452,7 +523,16 @@ struct C0Cycle {
         }
         __syncthreads();
         probe(0, PB + 1);
-        C0Cycle<NC>::run(cbase, lu, perm, pre, post);
+    }
+    // prolongation of the next level's x and post-smoothing
+    __device__ static void run_post(double* base, int post)
+    {
+        constexpr int NC = NX / 2;
+        constexpr int PB = 8 + 4 * (3 - DEPTH);
+        C0Level<NX> L;
+        layout(base, L);
+        C0Level<NC> Lc;
+        C0Cycle<NC>::layout(base + 13 * FullG<NX>::S, Lc);
         probe(0, PB + 2);
         for (int i = threadIdx.x; i < NX * NX; i += blockDim.x) {
             const int gy = i / NX, gx = i - gy * NX;
@@ -462,6 +542,13 @@ struct C0Cycle {
         __syncthreads();
         for (int s = 0; s < post; ++s) c0_sweep<false, NX>(L);
         probe(0, PB + 3);
+    }
+    __device__ __noinline__ static void run(double* base, const double* lu, const int* perm, int pre,
+                                            int post)
+    {
+        run_pre(base, pre);
+        C0Cycle<NX / 2>::run(base + 13 * FullG<NX>::S, lu, perm, pre, post);
+        run_post(base, post);
     }
 };
 
@@ -508,23 +595,31 @@ struct C0Cycle<3> { // level 2: dense 9x9 LU solve (DenseFactor::solve), factor 
 };
 
 // ----------------------------------------------------------- shared layout
+// TOP = 8: a constant-stencil (+ diagonal) level 8 in 16-row bands (4 nodes
+// per colour per thread; x in shared memory, b and 1/a_ii in registers) above
+// the level-7 structure. Level-8 residual rows share space with the level-7
+// and level-6 residuals (never live at the same time).
 template <int TOP>
 struct Lay {
-    using G0 = SlabG<(1 << TOP) - 1, TOP == 7 ? 8 : 4>; // top slab level
-    using G1 = SlabG<63, 4>;                             // level 6 below a level-7 top
-    static constexpr bool S1 = TOP == 7;
-    static constexpr int BARS = 0; // 8 mbarriers (4 per slab level)
-    static constexpr int X0 = BARS + 8;
-    static constexpr int R0 = X0 + G0::XS;
-    static constexpr int X1 = R0 + G0::RS;
-    static constexpr int R1 = X1 + (S1 ? G1::XS : 0);
-    static constexpr int C1 = R1 + (S1 ? G1::RS : 0); // coef [4 colours][9][GROUP1]
+    static constexpr bool S8 = TOP == 8;
+    static constexpr bool S1 = TOP >= 7;
+    using G8 = SlabG<255, 16, 4>;                        // level 8 (TOP = 8)
+    using G0 = SlabG<S1 ? 127 : 63, S1 ? 8 : 4>;         // level 7 (TOP 7, 8) or 6 (TOP 6)
+    using G1 = SlabG<63, 4>;                             // level 6 below a level-7 slab
+    static constexpr int BARS = 0;                       // 12 mbarriers (4 per slab level)
+    static constexpr int X8 = BARS + 12;
+    static constexpr int X0 = X8 + (S8 ? G8::XS : 0);
+    static constexpr int RT = X0 + G0::XS;               // residual rows
+    static constexpr int R0 = RT;
+    static constexpr int R1 = R0 + G0::RS;
+    static constexpr int RTS = (S8 && G8::RS > G0::RS + G1::RS) ? G8::RS : G0::RS + (S1 ? G1::RS : 0);
+    static constexpr int X1 = RT + RTS;
+    static constexpr int C1 = X1 + (S1 ? G1::XS : 0); // coef [4 colours][9][GROUP1]
     static constexpr int I1 = C1 + (S1 ? 36 * G1::GROUP : 0);
     static constexpr int B1 = I1 + (S1 ? 4 * G1::GROUP : 0);
     static constexpr int RED = B1 + (S1 ? 4 * G1::GROUP : 0); // cluster reduction slots
-    static constexpr int LU = RED + kCS;                      // 81 LU + 9 perm (as int)
-    static constexpr int C0BASE = LU + 96;                    // CTA-0 levels (31, 15, 7, 3)
-    static constexpr size_t total() { return (size_t)C0BASE + C0Cycle<31>::doubles(); }
+    static constexpr int C0BASE = RED + kCS;                  // CTA 0: level 5 + level-4 x, b
+    static constexpr size_t total() { return (size_t)C0BASE + 13 * FullG<31>::S + 2 * FullG<15>::S; }
 };
 
 template <int TOP>
@@ -533,10 +628,13 @@ __global__ void __launch_bounds__(kCT, 1)
                      int cycles, int pre, int post, int check, double* state, int* flags)
 {
     using Ly = Lay<TOP>;
+    using G8 = typename Ly::G8;
     using G0 = typename Ly::G0;
     using G1 = typename Ly::G1;
+    constexpr bool S8 = Ly::S8;
     constexpr int NX0 = G0::NX, RP0 = G0::RP;
     constexpr int NC = 31; // first CTA-0 level
+    constexpr int K0 = S8 ? 1 : 0; // ops index of the G0 level
     extern __shared__ double sm[];
     __shared__ double red[33];
     cg::cluster_group cl = cg::this_cluster();
@@ -546,6 +644,8 @@ __global__ void __launch_bounds__(kCT, 1)
     probe(w, 0);
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Ly::BARS);
+    double* x8 = sm + Ly::X8;
+    double* r8s = sm + Ly::RT;
     double* x0 = sm + Ly::X0;
     double* r0s = sm + Ly::R0;
     double* x1 = sm + Ly::X1;
@@ -553,28 +653,47 @@ __global__ void __launch_bounds__(kCT, 1)
     double* c1 = sm + Ly::C1;
     double* i1 = sm + Ly::I1;
     double* b1 = sm + Ly::B1;
-    double* lus = sm + Ly::LU;
-    int* perms = reinterpret_cast<int*>(lus + 81);
     double* c0base = sm + Ly::C0BASE;
     C0Level<NC> L5;
     C0Cycle<NC>::layout(c0base, L5);
 
+    const OwnM<G8> o8(w);
     const Own<G0> o0(w);
     const Own<G1> o1(w);
     Halo<G0> H0;
     H0.setup(bars, x0, w);
     Halo<G1> H1;
     H1.setup(bars + 4, x1, w);
+    Halo<G8> H8;
+    H8.setup(bars + 8, x8, w);
     if (threadIdx.x == 0) {
         H0.init_barriers();
         if constexpr (Ly::S1) H1.init_barriers();
+        if constexpr (S8) H8.init_barriers();
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
 
-    // ---- load: the top level's four rows per thread into registers, the rest into shared memory
+    // ---- load. Level 8: b and 1/a_ii of the thread's 16 nodes in registers.
+    double rb8[S8 ? G8::NPT : 1][4] = {}, ri8[S8 ? G8::NPT : 1][4] = {};
+    if constexpr (S8) {
+        const Op9& A = a.ops[0];
+#pragma unroll
+        for (int m = 0; m < G8::NPT; ++m)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                rb8[m][c] = ri8[m][c] = 0.0;
+                if (o8.valid(m, c)) {
+                    const long long gi = (long long)o8.gy(m, c) * G8::NX + o8.gx(m, c);
+                    rb8[m][c] = bg[gi];
+                    ri8[m][c] = 1.0 / (A.c[4] + (A.diag ? A.diag[gi] : 0.0)); // = k_inv_diag
+                }
+            }
+        for (int i = threadIdx.x; i < G8::XS; i += blockDim.x) x8[i] = 0.0;
+    }
+    // the G0 level's four nodes per thread: coefficients, 1/a_ii, b in registers
     double ra[4][9], rinv[4], rb[4];
     {
-        const Op9& A = a.ops[0];
+        const Op9& A = a.ops[K0];
         const long long n = (long long)NX0 * NX0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -583,7 +702,7 @@ __global__ void __launch_bounds__(kCT, 1)
 #pragma unroll
                 for (int d = 0; d < 9; ++d) ra[c][d] = op_entry(A, d, n, gi);
                 rinv[c] = 1.0 / ra[c][4];
-                rb[c] = bg[gi];
+                rb[c] = S8 ? 0.0 : bg[gi];
             } else {
 #pragma unroll
                 for (int d = 0; d < 9; ++d) ra[c][d] = 0.0;
@@ -593,7 +712,7 @@ __global__ void __launch_bounds__(kCT, 1)
         for (int i = threadIdx.x; i < G0::XS; i += blockDim.x) x0[i] = 0.0;
     }
     if constexpr (Ly::S1) {
-        const Op9& A = a.ops[1];
+        const Op9& A = a.ops[K0 + 1];
         const long long n = (long long)G1::NX * G1::NX;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -608,16 +727,24 @@ __global__ void __launch_bounds__(kCT, 1)
             }
         }
     }
-    if (w == 0) {
-        C0Cycle<NC>::load(c0base, a, Ly::S1 ? 2 : 1);
-        if (threadIdx.x < 81) lus[threadIdx.x] = a.lu[threadIdx.x];
-        if (threadIdx.x < 9) perms[threadIdx.x] = a.perm[threadIdx.x];
+    // levels <= 4: CTAs 1..15 hold 15 rows each of the dense level-4 V-cycle
+    // operator (k_coarse_op) where CTA 0 keeps level 5
+    double* cops = c0base;
+    if (w > 0) {
+        const double* src = a.cop + (size_t)kCopRows * kCopN * (w - 1);
+        for (int i = threadIdx.x; i < kCopRows * kCopN; i += blockDim.x) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(cops + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src + i) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    } else {
+        C0Cycle<NC>::load_top(c0base, a, K0 + (Ly::S1 ? 2 : 1));
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     }
     cl.sync();
     probe(w, 1);
 
-    // GS update of the thread's colour-c top-level node (register rows)
+    // GS update of the thread's colour-c G0 node (register rows)
     auto upd0 = [&](int c) -> double {
         double s = rb[c];
 #pragma unroll
@@ -636,6 +763,17 @@ __global__ void __launch_bounds__(kCT, 1)
         }
         return s * i1[o1.slot(c)];
     };
+    // level 8: constant stencil, the reference row order (k_sweep)
+    auto upd8 = [&](int m, int c) -> double {
+        const Op9& A = a.ops[0];
+        double s = rb8[m][c];
+#pragma unroll
+        for (int d = 0; d < 9; ++d) {
+            if (d == 4) continue;
+            s -= A.c[d] * x8[o8.q[m] + G8::nb(c, d % 3 - 1, d / 3 - 1)];
+        }
+        return s * ri8[m][c];
+    };
     // cluster-wide sum of per-thread values; the result is valid in CTA 0 thread 0
     auto cluster_sum = [&](double v) -> double {
         v = block_sum(v, red);
@@ -647,7 +785,7 @@ __global__ void __launch_bounds__(kCT, 1)
         cl.sync();
         return tot;
     };
-    // residual of the top level at the thread's nodes (stored for the restriction); returns sum r^2
+    // residual of the G0 level at the thread's nodes (stored for the restriction); returns sum r^2
     auto top_residual = [&]() -> double {
         H0.ensure_all();
         double r2 = 0.0;
@@ -664,16 +802,36 @@ __global__ void __launch_bounds__(kCT, 1)
         }
         return r2;
     };
+    // level-8 residual (k_resid_restrict's row order), stored row-major; returns sum r^2
+    auto residual8 = [&]() -> double {
+        H8.ensure_all();
+        const Op9& A = a.ops[0];
+        double r2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < G8::NPT; ++m)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (!o8.valid(m, c)) continue;
+                const long long gi = (long long)o8.gy(m, c) * G8::NX + o8.gx(m, c);
+                double s = 0.0;
+#pragma unroll
+                for (int d = 0; d < 9; ++d) {
+                    double av = A.c[d];
+                    if (d == 4 && A.diag) av += A.diag[gi];
+                    s += av * x8[o8.q[m] + G8::nb(c, d % 3 - 1, d / 3 - 1)];
+                }
+                const double r = rb8[m][c] - s;
+                r8s[(o8.gy(m, c) - G8::RP * w) * G8::NX + o8.gx(m, c)] = r;
+                r2 += r * r;
+            }
+        return r2;
+    };
     // prolongate a coarse correction into a slab level: own nodes, then the two
     // halo rows recomputed from the same parents (the neighbour does the same)
-    auto prolong_slab = [&](auto geo, double* xs, const auto& own, const auto& cxv) {
+    auto prolong_halo = [&](auto geo, double* xs, const auto& cxv) {
         using GG = decltype(geo);
         constexpr int NXF = GG::NX, RPF = GG::RP, NXC = NXF / 2;
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-            if (own.valid(c)) xs[own.me(c)] += prolong_from<NXC>(cxv, own.gx(c), own.gy(c));
-        const int t = threadIdx.x;
-        if (t < 2 * NXF) {
+        for (int t = threadIdx.x; t < 2 * NXF; t += blockDim.x) {
             const int gx = t % NXF, side = t / NXF;
             const int lr = side ? RPF + 1 : 0;
             const int gy = RPF * w + lr - 1;
@@ -681,17 +839,17 @@ __global__ void __launch_bounds__(kCT, 1)
         }
         cl.sync(); // neighbours finish reading their old halo values before new pushes
     };
-
-    double prev = 0.0;
-    if (check) {
-        double b2 = 0.0;
+    auto prolong_slab = [&](auto geo, double* xs, const auto& own, const auto& cxv) {
+        using GG = decltype(geo);
+        constexpr int NXC = GG::NX / 2;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) b2 += rb[c] * rb[c];
-        prev = sqrt(cluster_sum(b2));
-    }
+        for (int c = 0; c < 4; ++c)
+            if (own.valid(c)) xs[own.me(c)] += prolong_from<NXC>(cxv, own.gx(c), own.gy(c));
+        prolong_halo(geo, xs, cxv);
+    };
 
-    for (int cyc = 0; cyc < cycles; ++cyc) {
-        // ===================== top slab level: pre-smoothing, residual
+    // ===================== one V-cycle from the G0 level down (x0 holds its iterate)
+    auto cycle0 = [&]() {
         for (int s = 0; s < pre; ++s) slab_sweep<true>(x0, H0, o0, upd0);
         top_residual();
         cl.sync();
@@ -745,8 +903,33 @@ __global__ void __launch_bounds__(kCT, 1)
         }
         cl.sync();
         probe(w, 4);
-        // ===================== CTA-0 levels and the LU solve
-        if (w == 0) C0Cycle<NC>::run(c0base, lus, perms, pre, post);
+        // ===================== level 5 in CTA 0; levels <= 4 as x4 = B4 b4
+        if (w == 0) C0Cycle<NC>::run_pre(c0base, pre);
+        cl.sync();
+        if (w > 0) { // 15 rows per CTA, 16 lanes per row, DSM in and out
+            C0Level<NC / 2> L4;
+            C0Cycle<NC / 2>::layout(c0base + 13 * FullG<NC>::S, L4);
+            const double* b4 = cl.map_shared_rank(L4.b, 0);
+            double* x4 = cl.map_shared_rank(L4.x, 0);
+            double* b4l = cops + kCopRows * kCopN; // local copy of b4
+            for (int j = threadIdx.x; j < kCopN; j += blockDim.x) b4l[j] = b4[FullG<NC / 2>::xi(j % 15, j / 15)];
+            __syncthreads();
+            const int r = threadIdx.x >> 4, ch = threadIdx.x & 15;
+            double sum = 0.0;
+            if (r < kCopRows) {
+                const double* row = cops + r * kCopN;
+#pragma unroll 2
+                for (int j = ch; j < kCopN; j += 16) sum += row[j] * b4l[j];
+            }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (r < kCopRows && ch == 0) {
+                const int i = kCopRows * (w - 1) + r;
+                x4[FullG<NC / 2>::xi(i % 15, i / 15)] = sum;
+            }
+        }
+        cl.sync();
+        if (w == 0) C0Cycle<NC>::run_post(c0base, post);
         cl.sync();
         probe(w, 5);
         // ===================== prolongations and post-smoothing
@@ -757,7 +940,7 @@ __global__ void __launch_bounds__(kCT, 1)
                 prolong_slab(G1{}, x1, o1, cx5);
                 for (int s = 0; s < post; ++s) slab_sweep<false>(x1, H1, o1, upd1);
                 H1.ensure_all();
-                // level-7 parents lie in this CTA's level-6 band or its halo rows
+                // G0 parents lie in this CTA's level-6 band or its halo rows
                 auto cx6 = [&](int u, int v) { return x1[G1::xi(u, v - G1::RP * w + 1)]; };
                 prolong_slab(G0{}, x0, o0, cx6);
             } else {
@@ -767,16 +950,86 @@ __global__ void __launch_bounds__(kCT, 1)
         probe(w, 6);
         for (int s = 0; s < post; ++s) slab_sweep<false>(x0, H0, o0, upd0);
         probe(w, 7);
-        if (check) {
-            const double res = sqrt(cluster_sum(top_residual()));
-            if (w == 0 && threadIdx.x == 0 && res > 10.0 * prev) atomicOr(flags, kErrMgDiverged);
-            prev = res;
-        }
-        H0.ensure_all();
-    }
+    };
+
+    double prev = 0.0;
+    if (check) {
+        double b2 = 0.0;
+        if constexpr (S8) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-        if (o0.valid(c)) xg[(long long)o0.gy(c) * NX0 + o0.gx(c)] = x0[o0.me(c)];
+            for (int m = 0; m < G8::NPT; ++m)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) b2 += rb8[m][c] * rb8[m][c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) b2 += rb[c] * rb[c];
+        }
+        prev = sqrt(cluster_sum(b2));
+    }
+
+    for (int cyc = 0; cyc < cycles; ++cyc) {
+        if constexpr (S8) {
+            // ===================== level 8: pre-smoothing, residual, restriction into level 7
+            probe(w, 20);
+            for (int s = 0; s < pre; ++s) slab_sweep_m<true>(x8, H8, o8, upd8);
+            probe(w, 21);
+            residual8();
+            cl.sync();
+            probe(w, 22);
+            {
+                auto fr8 = [&](int gx, int gy) -> double {
+                    const int owner = gy / G8::RP;
+                    const double* rr = owner == w ? r8s : cl.map_shared_rank(r8s, (unsigned)owner);
+                    return rr[(gy - owner * G8::RP) * G8::NX + gx];
+                };
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    rb[c] = o0.valid(c) ? restrict_from(fr8, o0.gx(c), o0.gy(c)) : 0.0;
+                for (int i = threadIdx.x; i < G0::XS; i += blockDim.x) x0[i] = 0.0;
+            }
+            cl.sync(); // level-8 residual rows are free again (level-7 residual reuses them)
+            probe(w, 23);
+            cycle0();
+            H0.ensure_all();
+            probe(w, 24);
+            // ===================== prolongation into level 8 (own nodes + halo rows), post-smoothing
+            auto cx7 = [&](int u, int v) { return x0[G0::xi(u, v - G0::RP * w + 1)]; };
+#pragma unroll
+            for (int m = 0; m < G8::NPT; ++m)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (o8.valid(m, c)) x8[o8.me(m, c)] += prolong_from<127>(cx7, o8.gx(m, c), o8.gy(m, c));
+            prolong_halo(G8{}, x8, cx7);
+            probe(w, 25);
+            for (int s = 0; s < post; ++s) slab_sweep_m<false>(x8, H8, o8, upd8);
+            probe(w, 26);
+            if (check) {
+                const double res = sqrt(cluster_sum(residual8()));
+                if (w == 0 && threadIdx.x == 0 && res > 10.0 * prev) atomicOr(flags, kErrMgDiverged);
+                prev = res;
+            }
+            H8.ensure_all();
+        } else {
+            cycle0();
+            if (check) {
+                const double res = sqrt(cluster_sum(top_residual()));
+                if (w == 0 && threadIdx.x == 0 && res > 10.0 * prev) atomicOr(flags, kErrMgDiverged);
+                prev = res;
+            }
+            H0.ensure_all();
+        }
+    }
+    if constexpr (S8) {
+#pragma unroll
+        for (int m = 0; m < G8::NPT; ++m)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (o8.valid(m, c)) xg[(long long)o8.gy(m, c) * G8::NX + o8.gx(m, c)] = x8[o8.me(m, c)];
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (o0.valid(c)) xg[(long long)o0.gy(c) * NX0 + o0.gx(c)] = x0[o0.me(c)];
+    }
     if (check && state && w == 0 && threadIdx.x == 0) state[0] = prev;
     cl.sync(); // no CTA exits while a neighbour may still address its shared memory
 }
@@ -821,6 +1074,39 @@ void launch_top(cudaStream_t s, const BottomArgs& a, const double* b, double* x,
 }
 
 static_assert(Lay<7>::total() * sizeof(double) <= 220 * 1024, "cluster layout exceeds shared memory");
+static_assert(Lay<8>::total() * sizeof(double) + 33 * 8 + 4 <= 227 * 1024, "level-8 layout exceeds shared memory");
+static_assert((size_t)kCopRows * kCopN + kCopN <= C0Cycle<31>::doubles(), "dense operator slice exceeds the CTA-0 region");
+
+// Dense operator of the levels <= 4 of a V-cycle (zero initial guess, `pre` /
+// `post` 4-colour sweeps, LU at level 2): column j = the cycle applied to e_j,
+// by the same CTA-0 code the cluster kernel ran there. out[bt][i * 225 + j].
+// The cycle is linear in its right-hand side, so B4 b equals the cycle's
+// result up to the order of the final sums.
+__global__ void __launch_bounds__(64) k_coarse_op(BottomArgs a, int pre, int post, double* out)
+{
+    extern __shared__ double sm[];
+    constexpr int NX = 15;
+    using G = FullG<NX>;
+    const int j = blockIdx.x, bt = blockIdx.y, t = threadIdx.x;
+    if (t == 0) s_probe_on = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) a.ops[k].coef += (size_t)bt * 9 * a.ops[k].nx * a.ops[k].nx;
+    double* lus = sm + C0Cycle<NX>::doubles();
+    int* perms = reinterpret_cast<int*>(lus + 81);
+    C0Cycle<NX>::load(sm, a, 0);
+    for (int i = t; i < 81; i += blockDim.x) lus[i] = a.lu[81 * (size_t)bt + i];
+    if (t < 9) perms[t] = a.perm[9 * (size_t)bt + t];
+    C0Level<NX> L;
+    C0Cycle<NX>::layout(sm, L);
+    for (int i = t; i < G::S; i += blockDim.x) L.b[i] = 0.0;
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    if (t == 0) L.b[G::xi(j % NX, j / NX)] = 1.0;
+    __syncthreads();
+    C0Cycle<NX>::run(sm, lus, perms, pre, post);
+    for (int i = t; i < kCopN; i += blockDim.x)
+        out[(size_t)bt * kCopN * kCopN + (size_t)i * kCopN + j] = L.x[G::xi(i % NX, i / NX)];
+}
 
 } // namespace
 
@@ -833,7 +1119,7 @@ void cluster_probes(int enable, unsigned long long* out64)
 bool cluster_bottom_supported()
 {
     static const bool supported = [] {
-        bool ok = set_attrs<7>() && set_attrs<6>();
+        bool ok = set_attrs<7>() && set_attrs<6>() && set_attrs<8>();
         if (ok) {
             cudaLaunchAttribute at{};
             cudaLaunchConfig_t cfg = cluster_cfg<7>(nullptr, &at);
@@ -847,12 +1133,26 @@ bool cluster_bottom_supported()
     return supported;
 }
 
+void launch_coarse_op(cudaStream_t s, const BottomArgs& a, int batch, int pre, int post, double* out)
+{
+    if (a.ops[0].nx != 15 || a.ops[1].nx != 7 || !a.ops[0].coef || !a.ops[1].coef)
+        throw std::runtime_error("coarse operator: levels 4 and 3 (variable stencils) expected");
+    const size_t smem = (C0Cycle<15>::doubles() + 96) * sizeof(double);
+    static const bool attr = cudaFuncSetAttribute(k_coarse_op, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)smem) == cudaSuccess;
+    (void)attr;
+    note_launch();
+    k_coarse_op<<<dim3(kCopN, batch), 64, smem, s>>>(a, pre, post, out);
+}
+
 void launch_bottom_cluster(cudaStream_t s, const ClusterArgs& a, const double* b, double* x,
                            int cycles, int pre, int post, bool check, double* state, int* flags)
 {
-    if (a.ops[0].nx == 127) launch_top<7>(s, a, b, x, cycles, pre, post, check, state, flags);
+    if (a.ops[0].nx == 255 && !a.ops[0].coef)
+        launch_top<8>(s, a, b, x, cycles, pre, post, check, state, flags);
+    else if (a.ops[0].nx == 127) launch_top<7>(s, a, b, x, cycles, pre, post, check, state, flags);
     else if (a.ops[0].nx == 63) launch_top<6>(s, a, b, x, cycles, pre, post, check, state, flags);
-    else throw std::runtime_error("cluster bottom: top level must be 6 or 7");
+    else throw std::runtime_error("cluster bottom: top level must be 6, 7 or a constant-stencil 8");
 }
 
 } // namespace ocb

@@ -356,6 +356,7 @@ void sweep_tile(int id, cudaStream_t s, const Op9& A, const double* b, const dou
 } // namespace
 
 std::atomic<int> g_cluster_bottom{1};
+std::atomic<int> g_cluster_top8{1};
 std::atomic<int> g_sweep_tile{-1}; // tuning override: -1 auto, else tile id (see launch_sweep_tiled)
 std::atomic<int> g_sweep_fuse{2};  // sweeps fused per launch (measured best, profiles/r01/tuning.md)
 

@@ -21,7 +21,7 @@ struct MgLevelDev {
     double* b;       // level right-hand side (coarse levels only)
 };
 
-constexpr int kBottomMaxLevels = 6;   // levels 2..7 at most in the single-CTA solver
+constexpr int kBottomMaxLevels = 7;   // levels 2..8 at most (cluster kernel with a level-8 top)
 constexpr int kBottomTopLevel = 6;    // grid levels <= this run inside one CTA
 
 struct BottomArgs {
@@ -30,6 +30,7 @@ struct BottomArgs {
     Op9 ops[kBottomMaxLevels];         // [0] = top level of the bottom solver
     const double* lu;                  // 9x9 LU of the level-2 matrix (column-major)
     const int* perm;
+    const double* cop;                 // cluster kernel: dense levels <= 4 cycle operator (225 x 225)
 };
 
 // k_mg_tiled.cu: the smoothing sweep and the fused residual + restriction
@@ -39,6 +40,7 @@ struct BottomArgs {
 extern std::atomic<int> g_sweep_tile;
 extern std::atomic<int> g_cluster_bottom; // 1: levels <= 7 in the cluster kernel (default), 0: single-CTA bottom
 extern std::atomic<int> g_sweep_fuse;     // sweeps per launch in the V-cycle (1..5, temporal blocking)
+extern std::atomic<int> g_cluster_top8;   // 1: constant-stencil level-8 hierarchies run whole in the cluster kernel
 // inv = 1 / diag(A) precomputed per level (launch_inv_diag).
 void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                         const double* x, double* xo, bool forward, bool zero_init,
@@ -99,6 +101,11 @@ bool cluster_bottom_supported();
 void cluster_probes(int enable, unsigned long long* out64);
 void launch_bottom_cluster(cudaStream_t s, const ClusterArgs& a, const double* b, double* x,
                            int cycles, int pre, int post, bool check, double* state, int* flags);
+// Dense operator of the V-cycle below level 5 (levels 4, 3 and the level-2 LU)
+// for the cluster kernel: a.ops[0] = level 4, a.ops[1] = level 3 of batch
+// element 0 (elements are 9 n_k apart), lu/perm of element 0; out: batch x 225 x 225.
+constexpr int kCoarseOpN = 225;
+void launch_coarse_op(cudaStream_t s, const BottomArgs& a, int batch, int pre, int post, double* out);
 
 } // namespace ocb
 

@@ -9,6 +9,10 @@
 //   minres / gmres                 krylov.cpp:37-212
 #include "solver.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "assembly.hpp"
 
 #include <algorithm>
@@ -199,6 +203,9 @@ void Hierarchy::allocate(int level, int batch, int smoother)
     } else {
         mbox_.release();
     }
+    if (cluster_) cop_.resize((size_t)kCoarseOpN * kCoarseOpN * batch);
+    else cop_.release();
+    cop_pre_ = cop_post_ = -1;
     lu_.resize(81 * (size_t)batch);
     perm_.resize(9 * (size_t)batch);
     part_.resize(kNormBlocks);
@@ -227,6 +234,12 @@ Op9 Hierarchy::level_op(int k, int bt) const
 
 void Hierarchy::build(Ctx& c, const Op9& fine, long long fcs, long long fds)
 {
+    // a constant-stencil level-8 operator (heat time blocks) runs its whole
+    // solve in the cluster kernel (level 8 in 16-row bands)
+    if (cluster_) {
+        const int top = (level_ == 8 && !fine.coef && g_cluster_top8.load()) ? 8 : kClusterTopLevel;
+        kb_ = level_ > top ? level_ - top : 0;
+    }
     fine_ = fine;
     fine_coef_stride_ = fcs;
     fine_diag_stride_ = fds;
@@ -242,8 +255,22 @@ void Hierarchy::build(Ctx& c, const Op9& fine, long long fcs, long long fds)
     launch_check("multigrid build");
 }
 
+void Hierarchy::ensure_coarse_op(Ctx& c, int pre, int post)
+{
+    if (!cluster_ || (pre == cop_pre_ && post == cop_post_)) return;
+    BottomArgs a{};
+    a.nlev = 3;
+    for (int j = 0; j < 3; ++j) a.ops[j] = level_op(K_ - 2 + j, 0);
+    a.lu = lu_.get();
+    a.perm = perm_.get();
+    launch_coarse_op(c.stream, a, batch_, pre, post, cop_.get());
+    cop_pre_ = pre;
+    cop_post_ = post;
+}
+
 void Hierarchy::build_inv(Ctx& c)
 {
+    cop_pre_ = cop_post_ = -1; // every (re)build ends here
     for (int k = 0; k < kb_; ++k) {
         const Op9 a = level_op(k, 0);
         const long long cs = k == 0 ? fine_coef_stride_ : 9 * level_n(k);
@@ -256,6 +283,7 @@ void Hierarchy::build_inv(Ctx& c)
 void Hierarchy::build_rediscretized(Ctx& c, const Op9& fine, const std::vector<const double*>& base)
 {
     if (batch_ != 1) throw InvalidArgument("rediscretised hierarchies are not batched");
+    if (cluster_) kb_ = level_ > kClusterTopLevel ? level_ - kClusterTopLevel : 0;
     fine_ = fine;
     fine_coef_stride_ = fine_diag_stride_ = 0;
     if (rem_.size() != (size_t)K_ + 1) {
@@ -290,6 +318,7 @@ BottomArgs Hierarchy::bottom_args(int kfrom, int bt) const
     for (int j = 0; j < a.nlev; ++j) a.ops[j] = level_op(kfrom + j, bt);
     a.lu = lu_.get() + 81 * (size_t)bt;
     a.perm = perm_.get() + 9 * (size_t)bt;
+    a.cop = cluster_ ? cop_.get() + (size_t)kCoarseOpN * kCoarseOpN * bt : nullptr;
     return a;
 }
 
@@ -377,6 +406,7 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
 void Hierarchy::solve(Ctx& c, const double* b, double* x, const MgParams& p, int bt, int* flags)
 {
     const long long n = level_n(0);
+    ensure_coarse_op(c, p.pre, p.post); // no-op after Problem::setup_precond (graph capture safe)
     if (kb_ == 0) {
         if (cluster_)
             launch_bottom_cluster(c.stream, bottom_args(0, bt), b, x, p.cycles, p.pre, p.post,
@@ -801,6 +831,9 @@ void Problem::setup_precond(int kind, const oc_ipm_params& p)
             HF_.build(ctx, F);
         }
     }
+    // dense coarse-cycle operators of the cluster bottom, outside any captured apply
+    for (Hierarchy* h : {&Hheat_, &HL_, &Hleft_, &Hright_, &HF_, &HFT_})
+        if (h->built()) h->ensure_coarse_op(ctx, mg_.pre, mg_.post);
     setup_kind_ = kind;
     launch_check("preconditioner setup");
 }
@@ -1454,9 +1487,14 @@ void Problem::time_applies(int kind, int reps, double* kkt_ms, double* prec_ms)
     float a = 0.f;
     cudaEventElapsedTime(&a, ctx.ev0, ctx.ev1);
     cudaEventRecord(ctx.ev0, ctx.stream);
+    const auto h0 = std::chrono::steady_clock::now();
     for (int i = 0; i < reps; ++i) precond_apply(kind, kx2_.get(), kw_.get());
     cudaEventRecord(ctx.ev1, ctx.stream);
+    const auto h1 = std::chrono::steady_clock::now();
     ctx.sync();
+    if (std::getenv("OC_DEBUG_HOST_TIME")) // tuning aid: host enqueue time vs device time
+        std::fprintf(stderr, "precond apply host enqueue %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(h1 - h0).count() / reps);
     float b = 0.f;
     cudaEventElapsedTime(&b, ctx.ev0, ctx.ev1);
     *kkt_ms = a / reps;

@@ -156,7 +156,12 @@ public:
     void solve(Ctx& c, const double* b, double* x, const MgParams& p, int bt, int* flags);
     // one smoothing sweep on the fine level (in place through the scratch buffer)
     void smooth(Ctx& c, const double* b, double* x, bool forward, int bt);
+    // cluster bottom: (re)compute the dense levels <= 4 cycle operator for these
+    // sweep counts if stale (build() invalidates it); enqueued on c's stream
+    void ensure_coarse_op(Ctx& c, int pre, int post);
+    const double* coarse_op() const { return cluster_ ? cop_.get() : nullptr; }
     int depth() const { return K_; }
+    bool built() const { return built_; }
     int level() const { return level_; }
     int smoother() const { return smoother_; }
     // bumped whenever allocate() (re)allocates device buffers: captured graphs
@@ -187,6 +192,8 @@ private:
     std::vector<DVec> inv_;         // 1/diag per tiled level (k < kb_), batch-strided
     DVec lu_;
     DevArray<int> perm_;
+    DVec cop_;                      // cluster: batch x 225 x 225 dense levels <= 4 cycle operator
+    int cop_pre_ = -1, cop_post_ = -1; // sweep counts cop_ was computed for (-1: stale)
     DVec part_, state_;
     DevArray<unsigned> cnt_; // last-block counter of the fused divergence check
     bool built_ = false;

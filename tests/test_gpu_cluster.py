@@ -1,0 +1,83 @@
+"""Cluster-resident multigrid bottom (k_mg_cluster.cu): the dense operator of
+the V-cycle below level 5 and the whole-solve level-8 variant used by the heat
+time blocks, each against the launch-per-level path on the same data."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture()
+def lib():
+    from paper_1806_05896_b200 import _lib
+
+    L = _lib.load()
+    yield L
+    _lib.check(L.oc_set_tuning(b"cluster_bottom", 1))
+    _lib.check(L.oc_set_tuning(b"cluster_top8", 1))
+
+
+def _tune(lib, name, value):
+    from paper_1806_05896_b200 import _lib
+
+    _lib.check(lib.oc_set_tuning(name, value))
+
+
+@pytest.mark.parametrize("ell", [6, 7, 8])
+def test_cluster_bottom_matches_single_cta_levels(oc, ctx, lib, ell):
+    """Levels <= 7 in the 16-CTA cluster (levels <= 4 as one dense operator)
+    give the V-cycle of the single-CTA bottom up to rounding."""
+    L = oc.assemble9("poisson", ell)
+    L[4] += 1.0
+    b = np.random.default_rng(ell).uniform(-1, 1, L.shape[1])
+    out = {}
+    for cb in (0, 1):
+        _tune(lib, b"cluster_bottom", cb)
+        mg = oc.MgHierarchy(L, ell, ctx=ctx)
+        out[cb] = [mg.solve(b, cyc, 5, 5) for cyc in (1, 3)]
+    for a, c in zip(out[1], out[0]):
+        assert rel(a, c) <= 1e-13
+
+
+@pytest.mark.parametrize("pre,post", [(5, 5), (2, 3)])
+def test_coarse_operator_is_symmetric_for_symmetric_levels(oc, ctx, lib, pre, post):
+    """The levels <= 4 cycle (forward colours pre, backward post, exact level-2
+    solve) of a symmetric hierarchy is a symmetric operator when pre == post;
+    its columns are finite and it changes with the sweep counts."""
+    from paper_1806_05896_b200 import _lib
+
+    ell = 7
+    L = oc.assemble9("poisson", ell)
+    L[4] += 0.5
+    mg = oc.MgHierarchy(L, ell, ctx=ctx)
+    B = np.zeros((225, 225))
+    _lib.check(lib.oc_debug_coarse_op(mg.h, pre, post, B.ctypes.data))
+    assert np.isfinite(B).all() and np.abs(B).max() > 0
+    asym = np.abs(B - B.T).max() / np.abs(B).max()
+    if pre == post:
+        assert asym <= 1e-13
+    else:
+        assert asym > 1e-8
+
+
+def test_heat_level8_blocks_in_cluster_match_tiled(oc, ctx, lib):
+    """Heat time blocks (level 8, M + tau L + diag(mhat_k)) solved whole in the
+    cluster kernel reproduce the tiled level-8 path bit for bit."""
+    from paper_1806_05896_b200 import configs
+
+    c = dataclasses.replace(configs.C5, horizon=2 * configs.C5.tau)
+    res = {}
+    for top8 in (0, 1):
+        _tune(lib, b"cluster_top8", top8)
+        qp = oc.QpProblem(oc.ControlProblem(pde="heat", alpha=c.alpha, beta=c.beta, y_d=c.y_d(),
+                                            u_a=c.u_a, u_b=c.u_b, tau=c.tau, horizon=c.horizon),
+                          oc.Grid(c.level), ctx)
+        res[top8] = oc.ipm_solve(qp, oc.IpmParams(sigma=c.sigma, solver=c.solver))
+    a, b = res[1], res[0]
+    assert a.stats.converged and b.stats.converged
+    assert [i.lin_iters for i in a.stats.iterations] == [i.lin_iters for i in b.stats.iterations]
+    assert rel(a.u, b.u) <= 1e-13 and rel(a.state.y, b.state.y) <= 1e-13

@@ -31,7 +31,8 @@ __global__ void k_pass(double* out, long long* cyc, int passes)
             }
             x[me] = (ACC == 2 ? s - s2 : s) * 0.25;
         }
-        if (MODE != 1) __syncthreads();
+        if (MODE == 3) __syncwarp();
+        else if (MODE != 1) __syncthreads();
     }
     long long t1 = clock64();
     if (t == 0) cyc[0] = t1 - t0;
@@ -60,6 +61,16 @@ int main()
     run(k_pass<2, 256>, "barrier only");
     run(k_pass<0, 256, 2>, "full pass, 256 active, 2 accumulators");
     run(k_pass<0, 16, 2>, "full pass, 16 active, 2 accumulators");
+    auto runw = [&](auto kern, const char* name) {
+        for (int rep = 0; rep < 2; ++rep) {
+            kern<<<1, 32>>>(out, cyc, P);
+            cudaDeviceSynchronize();
+        }
+        printf("%-40s %.1f cyc/pass\n", name, (double)cyc[0] / P);
+    };
+    runw(k_pass<3, 32>, "one warp, syncwarp, 32 active");
+    runw(k_pass<3, 16>, "one warp, syncwarp, 16 active");
+    runw(k_pass<0, 32>, "one warp, syncthreads, 32 active");
     run(k_pass<1, 16, 2>, "no barrier, 16 active, 2 accumulators");
     return 0;
 }
