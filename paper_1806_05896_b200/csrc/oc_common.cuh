@@ -36,20 +36,40 @@ __device__ __forceinline__ double op_coef(const Op9& A, int d, long long i, long
 
 // (A x)_i with the reference's row summation order (csr_spmv, kernels.cpp:33-45).
 // x points at the level's field; gx, gy are 0-based interior coordinates.
+// Neighbours outside the interior read as 0 through predicated loads (no
+// divergent branches): fma(a, 0, s) == s, so the sum equals skipping them.
 __device__ __forceinline__ double op_apply_at(const Op9& A, const double* __restrict__ x, int gx,
                                               int gy)
 {
     const int nx = A.nx;
-    const long long n = (long long)nx * nx;
-    const long long i = (long long)gy * nx + gx;
+    const int n = nx * nx; // < 2^31 at every level
+    const int i = gy * nx + gx;
+    const bool hw = gx > 0, he = gx < nx - 1, hs = gy > 0, hn = gy < nx - 1;
+    double v[9];
+    v[0] = (hs && hw) ? x[i - nx - 1] : 0.0;
+    v[1] = hs ? x[i - nx] : 0.0;
+    v[2] = (hs && he) ? x[i - nx + 1] : 0.0;
+    v[3] = hw ? x[i - 1] : 0.0;
+    v[4] = x[i];
+    v[5] = he ? x[i + 1] : 0.0;
+    v[6] = (hn && hw) ? x[i + nx - 1] : 0.0;
+    v[7] = hn ? x[i + nx] : 0.0;
+    v[8] = (hn && he) ? x[i + nx + 1] : 0.0;
     double s = 0.0;
+    if (A.coef) {
 #pragma unroll
-    for (int d = 0; d < 9; ++d) {
-        const int jx = gx + d % 3 - 1, jy = gy + d / 3 - 1;
-        if (jx < 0 || jx >= nx || jy < 0 || jy >= nx) continue;
-        double a = op_coef(A, d, i, n);
-        if (d == 4 && A.diag) a += A.diag[i];
-        s += a * x[(long long)jy * nx + jx];
+        for (int d = 0; d < 9; ++d) {
+            double a = A.coef[d * n + i];
+            if (d == 4 && A.diag) a += A.diag[i];
+            s += a * v[d];
+        }
+    } else {
+#pragma unroll
+        for (int d = 0; d < 9; ++d) {
+            double a = A.c[d];
+            if (d == 4 && A.diag) a += A.diag[i];
+            s += a * v[d];
+        }
     }
     return s;
 }
