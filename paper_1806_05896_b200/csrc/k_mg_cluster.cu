@@ -276,14 +276,15 @@ __device__ __forceinline__ void slab_sweep(double* xs, Halo<G>& H, const Own<G>&
             H.ensure(0);
             H.ensure(1);
         }
-        const bool act = o.valid(c);
+        // every owning thread updates (warp-uniform): a position outside the
+        // domain has zero b, coefficients and 1/a_ii, so it rewrites its zero pad
         double v = 0.0;
-        if (act) {
+        if (o.thr) {
             v = upd(c);
             xs[o.me(c)] = v;
         }
         __syncthreads(); // CTA-local visibility; every halo read of this pass is done
-        if (act) H.push(o, v, c);
+        if (o.valid(c)) H.push(o, v, c);
         H.passed(c);
     }
 }
@@ -302,12 +303,11 @@ __device__ __forceinline__ void slab_sweep_m(double* xs, Halo<G>& H, const OwnM<
             H.ensure(0);
             H.ensure(1);
         }
-        double v[G::NPT];
+        double v[G::NPT]; // positions outside the domain compute 0 (zero b and 1/a_ii)
 #pragma unroll
-        for (int m = 0; m < G::NPT; ++m) v[m] = o.valid(m, c) ? upd(m, c) : 0.0;
+        for (int m = 0; m < G::NPT; ++m) v[m] = upd(m, c);
 #pragma unroll
-        for (int m = 0; m < G::NPT; ++m)
-            if (o.valid(m, c)) xs[o.me(m, c)] = v[m];
+        for (int m = 0; m < G::NPT; ++m) xs[o.me(m, c)] = v[m];
         __syncthreads();
 #pragma unroll
         for (int m = 0; m < G::NPT; ++m)
@@ -724,6 +724,11 @@ __global__ void __launch_bounds__(kCT, 1)
                     c1[(c * 9 + d) * G1::GROUP + threadIdx.x] = v;
                     if (d == 4) i1[o1.slot(c)] = 1.0 / v;
                 }
+            } else if (o1.thr) { // outside the domain: zero row (branch-free sweeps)
+#pragma unroll
+                for (int d = 0; d < 9; ++d) c1[(c * 9 + d) * G1::GROUP + threadIdx.x] = 0.0;
+                i1[o1.slot(c)] = 0.0;
+                b1[o1.slot(c)] = 0.0;
             }
         }
     }
