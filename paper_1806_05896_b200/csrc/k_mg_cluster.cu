@@ -224,14 +224,17 @@ struct Halo {
             mbar_expect(bar + 8 * c, G::seg_bytes(c));
         }
     }
-    __device__ __forceinline__ void ensure(int c)
+    // consume the pending colour-c exchange: every thread keeps the phase
+    // bookkeeping, only `waiter` threads (those reading that halo row) spin on
+    // the mbarrier, and one of them (`armer`) re-arms the next phase
+    __device__ __forceinline__ void ensure(int c, bool waiter = true, bool armer = threadIdx.x == 0)
     {
         if (!((pend >> c) & 1u)) return;
         pend &= ~(1u << c);
         if (!(c < 2 ? has_dn() : has_up())) return;
-        mbar_wait(bar + 8 * c, (par >> c) & 1u);
+        if (waiter) mbar_wait(bar + 8 * c, (par >> c) & 1u);
         par ^= 1u << c;
-        if (threadIdx.x == 0) mbar_expect(bar + 8 * c, G::seg_bytes(c));
+        if (armer) mbar_expect(bar + 8 * c, G::seg_bytes(c));
     }
     __device__ __forceinline__ void ensure_all()
     {
@@ -269,17 +272,20 @@ __device__ __forceinline__ void slab_sweep(double* xs, Halo<G>& H, const Own<G>&
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const int c = FWD ? p : 3 - p;
-        if (c < 2) { // first-row nodes read the upper halo (colours 2, 3)
-            H.ensure(2);
-            H.ensure(3);
-        } else { // last-row nodes read the lower halo (colours 0, 1)
-            H.ensure(0);
-            H.ensure(1);
-        }
+        // first-row nodes read the upper halo (colours 2, 3), last-row nodes the
+        // lower one (colours 0, 1); the other rows update without waiting
+        const bool edge = c < 2 ? o.rr == 0 : o.rr == G::RH - 1;
+        const bool armer = edge && o.cc == 0;
         // every owning thread updates (warp-uniform): a position outside the
         // domain has zero b, coefficients and 1/a_ii, so it rewrites its zero pad
         double v = 0.0;
-        if (o.thr) {
+        if (o.thr && !edge) {
+            v = upd(c);
+            xs[o.me(c)] = v;
+        }
+        H.ensure(c < 2 ? 2 : 0, edge, armer);
+        H.ensure(c < 2 ? 3 : 1, edge, armer);
+        if (o.thr && edge) {
             v = upd(c);
             xs[o.me(c)] = v;
         }
@@ -296,13 +302,10 @@ __device__ __forceinline__ void slab_sweep_m(double* xs, Halo<G>& H, const OwnM<
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const int c = FWD ? p : 3 - p;
-        if (c < 2) {
-            H.ensure(2);
-            H.ensure(3);
-        } else {
-            H.ensure(0);
-            H.ensure(1);
-        }
+        // (waiting only in the edge warps and updating the other positions first,
+        // as slab_sweep does, costs registers here and measured slower)
+        H.ensure(c < 2 ? 2 : 0);
+        H.ensure(c < 2 ? 3 : 1);
         double v[G::NPT]; // positions outside the domain compute 0 (zero b and 1/a_ii)
 #pragma unroll
         for (int m = 0; m < G::NPT; ++m) v[m] = upd(m, c);
