@@ -2,7 +2,9 @@
 BASELINE config: one Newton step to set the preconditioner up, then
 oc_time_applies (warm-ups + `reps` timed applies).
 
-    python tools/profile_apply.py C4 [reps=1]
+    python tools/profile_apply.py C4 [reps=1] [smoother=color4]
+
+A config name may carry a level, e.g. C3@8.
 """
 import os
 import sys
@@ -13,7 +15,9 @@ from paper_1806_05896_b200 import configs, optcon as oc  # noqa: E402
 KIND = {"gmres-pt": "pt", "minres-pd": "pd", "gmres-ppi": "ppi"}
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-c = configs.ALL[name]
+smoother = sys.argv[3] if len(sys.argv) > 3 else "color4"
+base, _, lvl = name.partition("@")
+c = configs.ALL[base].with_level(int(lvl)) if lvl else configs.ALL[base]
 kw = dict(pde=c.pde, alpha=c.alpha, beta=c.beta, y_d=c.y_d(), u_a=c.u_a, u_b=c.u_b)
 if c.pde == "convdiff":
     kw["eps"] = c.eps
@@ -27,7 +31,7 @@ ctx = oc.Context(0)
 qp = oc.QpProblem(oc.ControlProblem(**kw), oc.Grid(c.level), ctx)
 try:
     oc.ipm_solve(qp, oc.IpmParams(sigma=c.sigma, solver=c.solver, max_iterations=1,
-                                  gmres_restart=c.gmres_restart))
+                                  gmres_restart=c.gmres_restart, smoother=smoother))
 except Exception as e:  # one IPM iteration does not converge: expected
     print("solve:", type(e).__name__, e)
 print("MARK apply start", flush=True)
