@@ -1124,20 +1124,30 @@ void cluster_probes(int enable, unsigned long long* out64)
     if (out64) cudaMemcpyFromSymbol(out64, g_tprobe, 64 * sizeof(unsigned long long));
 }
 
+template <int TOP>
+bool cluster_launchable()
+{
+    bool ok = set_attrs<TOP>();
+    if (ok) {
+        cudaLaunchAttribute at{};
+        cudaLaunchConfig_t cfg = cluster_cfg<TOP>(nullptr, &at);
+        int nclusters = 0;
+        ok = cudaOccupancyMaxActiveClusters(&nclusters, k_bottom_cluster<TOP>, &cfg) == cudaSuccess &&
+             nclusters > 0;
+    }
+    cudaGetLastError();
+    return ok;
+}
+
 bool cluster_bottom_supported()
 {
-    static const bool supported = [] {
-        bool ok = set_attrs<7>() && set_attrs<6>() && set_attrs<8>();
-        if (ok) {
-            cudaLaunchAttribute at{};
-            cudaLaunchConfig_t cfg = cluster_cfg<7>(nullptr, &at);
-            int nclusters = 0;
-            ok = cudaOccupancyMaxActiveClusters(&nclusters, k_bottom_cluster<7>, &cfg) == cudaSuccess &&
-                 nclusters > 0;
-        }
-        cudaGetLastError();
-        return ok;
-    }();
+    static const bool supported = cluster_launchable<7>() && cluster_launchable<6>();
+    return supported;
+}
+
+bool cluster_top8_supported()
+{
+    static const bool supported = cluster_bottom_supported() && cluster_launchable<8>();
     return supported;
 }
 

@@ -97,6 +97,7 @@ void launch_add9(cudaStream_t s, long long m, const double* a, const double* b, 
 using ClusterArgs = BottomArgs;
 constexpr int kClusterTopLevel = 7;
 bool cluster_bottom_supported();
+bool cluster_top8_supported(); // the level-8 (constant stencil + diagonal) variant fits this device
 // tuning aid: enable %globaltimer phase probes; read the last launch's stamps
 void cluster_probes(int enable, unsigned long long* out64);
 void launch_bottom_cluster(cudaStream_t s, const ClusterArgs& a, const double* b, double* x,

@@ -237,7 +237,9 @@ void Hierarchy::build(Ctx& c, const Op9& fine, long long fcs, long long fds)
     // a constant-stencil level-8 operator (heat time blocks) runs its whole
     // solve in the cluster kernel (level 8 in 16-row bands)
     if (cluster_) {
-        const int top = (level_ == 8 && !fine.coef && g_cluster_top8.load()) ? 8 : kClusterTopLevel;
+        const int top = (level_ == 8 && !fine.coef && g_cluster_top8.load() && cluster_top8_supported())
+                            ? 8
+                            : kClusterTopLevel;
         kb_ = level_ > top ? level_ - top : 0;
     }
     fine_ = fine;
