@@ -406,6 +406,7 @@ int oc_set_tuning(const char* name, int value)
         else if (k == "sweep_fuse") ocb::g_sweep_fuse = value;
         else if (k == "cluster_bottom") ocb::g_cluster_bottom = value;
         else if (k == "cluster_top8") ocb::g_cluster_top8 = value;
+        else if (k == "colour_split") ocb::g_colour_split = value;
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
     });
 }
@@ -420,6 +421,7 @@ int oc_get_tuning(const char* name, int* value)
         else if (k == "sweep_fuse") *value = ocb::g_sweep_fuse;
         else if (k == "cluster_bottom") *value = ocb::g_cluster_bottom;
         else if (k == "cluster_top8") *value = ocb::g_cluster_top8;
+        else if (k == "colour_split") *value = ocb::g_colour_split;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);
     });
 }

@@ -188,8 +188,12 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
 #pragma unroll
                 for (int d = 0; d < 9; ++d) {
                     if (d == 4) continue;
-                    const double a = S::CS ? cs[(d < 4 ? d : d - 1) * R + l]
-                                           : (VAR ? __ldg(cp + cpo[d]) : A.c[d]);
+                    double a;
+                    if (S::CS) a = cs[(d < 4 ? d : d - 1) * R + l];
+                    else if (VAR) a = A.csplit ? __ldg(A.csplit + (long long)(d < 4 ? d : d - 1) * n + gy * nx +
+                                                       ((gx & 1) ? ((nx + 1) >> 1) + (gx >> 1) : (gx >> 1)))
+                                               : __ldg(cp + cpo[d]);
+                    else a = A.c[d];
                     s -= a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
                 }
                 xs[l] = s * iv[l];
@@ -300,6 +304,19 @@ __global__ void __launch_bounds__(256) k_resid_restrict(Op9 A, const double* __r
     }
 }
 
+// colour-split copy of the off-diagonal planes: row y holds its even-x nodes,
+// then its odd-x nodes, so one colour pass of the tiled sweep reads whole sectors
+__global__ void k_colour_split(int nx, const double* __restrict__ coef, double* __restrict__ out)
+{
+    const long long n = (long long)nx * nx;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int gy = (int)(i / nx), gx = (int)(i - (long long)gy * nx);
+    const long long o = (long long)gy * nx + ((gx & 1) ? ((nx + 1) >> 1) + (gx >> 1) : (gx >> 1));
+    const int p = blockIdx.y, d = p < 4 ? p : p + 1;
+    out[p * n + o] = coef[d * n + i];
+}
+
 __global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long long fds)
 {
     const long long n = (long long)A.nx * A.nx;
@@ -359,6 +376,15 @@ std::atomic<int> g_cluster_bottom{1};
 std::atomic<int> g_cluster_top8{1};
 std::atomic<int> g_sweep_tile{-1}; // tuning override: -1 auto, else tile id (see launch_sweep_tiled)
 std::atomic<int> g_sweep_fuse{2};  // sweeps fused per launch (measured best, profiles/r01/tuning.md)
+
+std::atomic<int> g_colour_split{1};
+
+void launch_colour_split(cudaStream_t s, int nx, const double* coef, double* out)
+{
+    const long long n = (long long)nx * nx;
+    note_launch();
+    k_colour_split<<<dim3((unsigned)((n + 255) / 256), 8), 256, 0, s>>>(nx, coef, out);
+}
 
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
                      long long fds)

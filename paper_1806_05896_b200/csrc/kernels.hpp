@@ -47,6 +47,9 @@ void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const dou
                         const double* ec, int ns);
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
                      long long fds);
+// colour-split copy (Op9::csplit) of a variable operator's 8 off-diagonal planes
+extern std::atomic<int> g_colour_split; // 1: the fine level of >= 1023^2 hierarchies sweeps from it
+void launch_colour_split(cudaStream_t s, int nx, const double* coef, double* out);
 void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, const double* x,
                                  double* bc, double* xc);
 // x += P ec

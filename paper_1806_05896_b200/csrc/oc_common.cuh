@@ -22,6 +22,8 @@ struct Op9 {
     double c[9];          // constant stencil (when coef == nullptr)
     const double* diag;   // optional added diagonal (plus_diagonal), or nullptr
     double cscale;        // constant stencil multiplier (1 unless stated)
+    const double* csplit; // optional colour-split copy of the 8 off-diagonal planes
+                          // (row y: even x first, then odd x) read by the tiled sweep
 };
 
 constexpr int kRedBlocks = 296;   // fixed reduction grid: 2 x 148 SMs (deterministic)

@@ -222,6 +222,7 @@ Op9 Hierarchy::level_op(int k, int bt) const
         Op9 a = fine_;
         if (a.coef) a.coef += bt * fine_coef_stride_;
         if (a.diag) a.diag += bt * fine_diag_stride_;
+        a.csplit = bt == 0 && split_.size() > 0 && split_[0] ? split_[0].get() : nullptr;
         return a;
     }
     Op9 a{};
@@ -229,6 +230,7 @@ Op9 Hierarchy::level_op(int k, int bt) const
     a.coef = coef_[k].get() + (size_t)bt * 9 * level_n(k);
     a.diag = nullptr;
     a.cscale = 1.0;
+    a.csplit = bt == 0 && (size_t)k < split_.size() && split_[k] ? split_[k].get() : nullptr;
     return a;
 }
 
@@ -253,6 +255,7 @@ void Hierarchy::build(Ctx& c, const Op9& fine, long long fcs, long long fds)
                    9 * level_n(k + 1));
     }
     launch_coarse_lu(c.stream, coef_[K_].get(), lu_.get(), perm_.get(), batch_);
+    build_split(c);
     build_inv(c);
     launch_check("multigrid build");
 }
@@ -268,6 +271,29 @@ void Hierarchy::ensure_coarse_op(Ctx& c, int pre, int post)
     launch_coarse_op(c.stream, a, batch_, pre, post, cop_.get());
     cop_pre_ = pre;
     cop_post_ = post;
+}
+
+void Hierarchy::build_split(Ctx& c)
+{
+    // tiled variable levels of >= 511^2 nodes sweep from colour-split copies
+    // of their off-diagonals (one colour pass reads whole sectors); refreshed
+    // at every build, as the coarse levels change with each Newton step
+    const bool on = g_colour_split.load() && !lex_ && batch_ == 1;
+    if (split_.size() != (size_t)K_ + 1) {
+        split_.clear();
+        split_.resize(K_ + 1);
+    }
+    for (int k = 0; k <= K_; ++k) {
+        const double* src = k == 0 ? fine_.coef : coef_[k].get();
+        const double* before = split_[k].get();
+        if (!on || k >= kb_ || !src || nx_[k] < 500) {
+            split_[k].release();
+        } else {
+            split_[k].resize(8 * (size_t)level_n(k));
+            launch_colour_split(c.stream, nx_[k], src, split_[k].get());
+        }
+        if (split_[k].get() != before) ++gen_; // captured graphs hold the old pointers
+    }
 }
 
 void Hierarchy::build_inv(Ctx& c)
@@ -307,6 +333,7 @@ void Hierarchy::build_rediscretized(Ctx& c, const Op9& fine, const std::vector<c
         rem.coef = rem_[k + 1].get();
     }
     launch_coarse_lu(c.stream, coef_[K_].get(), lu_.get(), perm_.get(), 1);
+    build_split(c);
     build_inv(c);
     launch_check("multigrid build (rediscretised)");
 }

@@ -175,6 +175,7 @@ private:
                 int bt, int* flags);
     BottomArgs bottom_args(int kfrom, int bt) const;
     void build_inv(Ctx& c);
+    void build_split(Ctx& c);
     const double* inv_at(int k, int bt) const { return inv_[k].get() + (size_t)bt * level_n(k); }
 
     int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1, smoother_ = OC_SMOOTHER_COLOR4;
@@ -192,6 +193,7 @@ private:
     std::vector<DVec> inv_;         // 1/diag per tiled level (k < kb_), batch-strided
     DVec lu_;
     DevArray<int> perm_;
+    std::vector<DVec> split_;       // [k] colour-split off-diagonals of variable tiled levels >= 511^2 (batch 1)
     DVec cop_;                      // cluster: batch x 225 x 225 dense levels <= 4 cycle operator
     int cop_pre_ = -1, cop_post_ = -1; // sweep counts cop_ was computed for (-1: stale)
     DVec part_, state_;

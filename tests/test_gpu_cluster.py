@@ -83,3 +83,21 @@ def test_heat_level8_blocks_in_cluster_match_tiled(oc, ctx, lib, solver):
     assert a.stats.converged and b.stats.converged
     assert [i.lin_iters for i in a.stats.iterations] == [i.lin_iters for i in b.stats.iterations]
     assert rel(a.u, b.u) <= 1e-13 and rel(a.state.y, b.state.y) <= 1e-13
+
+
+def test_colour_split_coefficients_give_identical_sweeps(oc, ctx, lib):
+    """Tiled sweeps reading the colour-split copy of the off-diagonals (levels
+    >= 511^2) reproduce the canonical-layout sweeps bit for bit."""
+    ell = 10
+    L = oc.assemble9("convdiff", ell, eps=0.02)
+    L[4] += 1.0
+    b = np.random.default_rng(7).uniform(-1, 1, L.shape[1])
+    out = {}
+    try:
+        for v in (0, 1):
+            _tune(lib, b"colour_split", v)
+            mg = oc.MgHierarchy(L, ell, rediscretize=1, eps=0.02, ctx=ctx)
+            out[v] = mg.solve(b, 2, 5, 5)
+    finally:
+        _tune(lib, b"colour_split", 1)
+    assert np.array_equal(out[0], out[1])

@@ -19,6 +19,9 @@ while args[:1] and args[0].startswith("--"):
     flag, val, args = args[0], args[1], args[2:]
     if flag == "--smoother":
         smoother = val
+    elif flag == "--tune":  # name=value, any oc_set_tuning knob
+        key, v = val.split("=")
+        _lib.check(_lib.load().oc_set_tuning(key.encode(), int(v)))
     elif flag in ("--fuse", "--tile"):
         key = b"sweep_fuse" if flag == "--fuse" else b"sweep_tile"
         _lib.check(_lib.load().oc_set_tuning(key, int(val)))
