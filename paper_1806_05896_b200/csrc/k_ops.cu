@@ -6,6 +6,8 @@
 // reference's evaluation order term by term so results agree to rounding.
 #include "kernels.hpp"
 
+#include <algorithm>
+
 namespace ocb {
 
 namespace {
@@ -186,6 +188,89 @@ __global__ void k_cheb_step(ProbDev P, const double* __restrict__ e, double omeg
     next[g] = wk * (s_cur + gv[g] - pv) + pv;
 }
 
+// Up to kChebTS Chebyshev steps in one launch (temporal blocking): a CTA
+// stages the previous two iterates, g and e over its 32x32 tile plus a halo of
+// kChebTS nodes in shared memory and advances the region (shrinking by one
+// ring per step) in place, the update being k_cheb_step's expressions in the
+// same order (cells outside the domain hold 0, as op_apply_at's predicated
+// loads read): results equal the step-by-step launches bit for bit. Writes
+// the last two iterates of the tile.
+constexpr int kChebTS = 5, kChebT = 32, kChebR = kChebT + 2 * kChebTS;
+struct ChebSteps {
+    double wk[kChebTS];
+    int st0, nst; // first step index (>= 2) and steps in this launch
+};
+
+__global__ void __launch_bounds__(256) k_cheb_block(ProbDev P, const double* __restrict__ e, double omega,
+                                                    ChebSteps S, const double* __restrict__ prev,
+                                                    const double* __restrict__ cur,
+                                                    const double* __restrict__ gv,
+                                                    double* __restrict__ out_prev,
+                                                    double* __restrict__ out_cur)
+{
+    constexpr int R = kChebR, RR = R * R;
+    extern __shared__ double csm[];
+    double* yp = csm;
+    double* yc = yp + RR;
+    double* gs = yc + RR;
+    double* es = gs + RR;
+    const int nx = P.nx, k = blockIdx.z;
+    const long long off = (long long)k * P.ns;
+    const int tx0 = blockIdx.x * kChebT, ty0 = blockIdx.y * kChebT;
+    const int ox = tx0 - kChebTS, oy = ty0 - kChebTS;
+    for (int l = threadIdx.x; l < RR; l += blockDim.x) {
+        const int gy = oy + l / R, gx = ox + l % R;
+        double a = 0.0, c = 0.0, gg = 0.0, ee = 0.0;
+        if (gx >= 0 && gx < nx && gy >= 0 && gy < nx) {
+            const long long g = off + (long long)gy * nx + gx;
+            a = prev ? prev[g] : 0.0;
+            c = cur[g];
+            gg = gv[g];
+            ee = e ? e[g] : 0.0;
+        }
+        yp[l] = a;
+        yc[l] = c;
+        gs[l] = gg;
+        es[l] = ee;
+    }
+    __syncthreads();
+    const double sk = P.heat ? P.tau * P.qw[k] : 1.0;
+    double* pa = yp;
+    double* pc = yc;
+    for (int i = 0; i < S.nst; ++i) {
+        const int st = S.st0 + i;
+        const double wk = S.wk[i];
+        const int lo = i + 1, hi = R - i - 1; // region rows/columns still exact after this step
+        for (int l = threadIdx.x; l < RR; l += blockDim.x) {
+            const int ly = l / R, lx = l - ly * R;
+            const int gy = oy + ly, gx = ox + lx;
+            if (ly < lo || ly >= hi || lx < lo || lx >= hi || gx < 0 || gx >= nx || gy < 0 || gy >= nx) continue;
+            double az = 0.0;
+#pragma unroll
+            for (int d = 0; d < 9; ++d) az += P.M.c[d] * pc[l + (d / 3 - 1) * R + (d % 3 - 1)];
+            if (P.heat) az = (P.tau * P.qw[k]) * az;
+            if (e) az += es[l] * pc[l];
+            const double invd = 1.0 / (sk * P.M.c[4] + (e ? es[l] : 0.0));
+            const double s_cur = pc[l] - omega * invd * az;
+            const double pv = st == 2 ? 0.0 : pa[l];
+            pa[l] = wk * (s_cur + gs[l] - pv) + pv;
+        }
+        __syncthreads();
+        double* t = pa;
+        pa = pc;
+        pc = t;
+    }
+    for (int l = threadIdx.x; l < kChebT * kChebT; l += blockDim.x) {
+        const int ly = l / kChebT, lx = l - ly * kChebT;
+        const int gy = ty0 + ly, gx = tx0 + lx;
+        if (gx >= nx || gy >= nx) continue;
+        const long long g = off + (long long)gy * nx + gx;
+        const int q = (ly + kChebTS) * R + lx + kChebTS;
+        if (out_prev) out_prev[g] = pa[q];
+        out_cur[g] = pc[q];
+    }
+}
+
 // ------------------------------------------------------------------ 2x2 block
 __global__ void k_control_2x2(ProbDev P, const double* __restrict__ tw,
                               const double* __restrict__ tv, const double* __restrict__ rw,
@@ -357,6 +442,8 @@ void launch_kkt(cudaStream_t s, const ProbDev& P, const double* ty, const double
     }
 }
 
+std::atomic<int> g_cheb_block{1};
+
 void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const double* e,
                       int steps, const ChebWork& w, double* out)
 {
@@ -371,6 +458,38 @@ void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const d
     }
     note_launch();
     k_cheb_init<<<grid, kT, 0, s>>>(P, b, e, omega, w.g);
+    if (g_cheb_block.load(std::memory_order_relaxed)) {
+        // kChebTS steps per launch; the chunks' (previous, current) iterate
+        // pairs alternate between (r0, r1) and (r2, out), the last chunk's
+        // landing in (r2, out)
+        const int nchunk = (steps - 1 + kChebTS - 1) / kChebTS;
+        const dim3 bgrid((P.nx + kChebT - 1) / kChebT, (P.nx + kChebT - 1) / kChebT, P.nt);
+        const double* prev = nullptr;
+        const double* cur = w.g;
+        double wk = 1.0;
+        int st = 2;
+        for (int c = 0; c < nchunk; ++c) {
+            const bool pairB = (nchunk - 1 - c) % 2 == 0;
+            double* op = pairB ? w.r2 : w.r0;
+            double* oc = pairB ? out : w.r1;
+            ChebSteps S{};
+            S.st0 = st;
+            S.nst = std::min(kChebTS, steps - st + 1);
+            for (int i = 0; i < S.nst; ++i, ++st) {
+                wk = (st == 2) ? 1.0 / (1.0 - 0.5 * rho * rho) : 1.0 / (1.0 - 0.25 * rho * rho * wk);
+                S.wk[i] = wk;
+            }
+            constexpr size_t smem = 4 * (size_t)kChebR * kChebR * sizeof(double);
+            static const bool attr = cudaFuncSetAttribute(k_cheb_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                          (int)smem) == cudaSuccess;
+            (void)attr;
+            note_launch();
+            k_cheb_block<<<bgrid, 256, smem, s>>>(P, e, omega, S, prev, cur, w.g, op, oc);
+            prev = op;
+            cur = oc;
+        }
+        return;
+    }
     // rotating buffers R[s % 3]; the last step (s = steps) writes into out
     double* R[3] = {w.r0, w.r1, w.r2};
     R[steps % 3] = out;

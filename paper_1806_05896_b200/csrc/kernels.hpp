@@ -150,6 +150,7 @@ struct ChebWork {
 };
 void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const double* e,
                       int steps, const ChebWork& w, double* out);
+extern std::atomic<int> g_cheb_block; // 1: up to 5 Chebyshev steps per launch (temporal blocking)
 
 // 2x2 control block inverse (precond.cpp:37-53, 148-157; heat timedep.cpp:383-393)
 void launch_control_2x2(cudaStream_t s, const ProbDev& P, const double* tw, const double* tv,

@@ -101,3 +101,28 @@ def test_colour_split_coefficients_give_identical_sweeps(oc, ctx, lib):
     finally:
         _tune(lib, b"colour_split", 1)
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("pde", ["poisson", "heat"])
+def test_blocked_chebyshev_equals_stepwise(oc, ctx, lib, pde):
+    """Five Chebyshev steps per launch (temporal blocking over 32x32 tiles)
+    reproduce the one-step-per-launch semi-iteration bit for bit."""
+    from paper_1806_05896_b200 import configs
+
+    c = configs.C5 if pde == "heat" else configs.C1
+    kw = dict(pde=pde, alpha=c.alpha, beta=c.beta, u_a=c.u_a, u_b=c.u_b)
+    level = 6
+    if pde == "heat":
+        kw.update(tau=c.tau, horizon=3 * c.tau)
+        kw["y_d"] = configs.sine_modes_spacetime(level, 3, c.tau, 42)
+    else:
+        kw["y_d"] = configs.sine_modes(level, seed=42)
+    out = {}
+    try:
+        for v in (0, 1):
+            _tune(lib, b"cheb_block", v)
+            qp = oc.QpProblem(oc.ControlProblem(**kw), oc.Grid(level), ctx)
+            out[v] = oc.ipm_solve(qp, oc.IpmParams(sigma=0.2, solver="gmres-pt")).u
+    finally:
+        _tune(lib, b"cheb_block", 1)
+    assert np.array_equal(out[0], out[1])
