@@ -80,31 +80,6 @@ __global__ void k_prolong_add(int nx, const double* __restrict__ ec, double* __r
     x[i] = x[i] + prolong_at(ec, (nx - 1) / 2, gx, gy);
 }
 
-// The block that completes last sums the partials (fixed order) and applies
-// the divergence check of MgHierarchy::solve (multigrid.cpp:141-157):
-// res = sqrt(sum); flag if res > 10 state[0] (unless init); state[0] = res.
-// Every block fences its partial before counting, the last one reads them
-// through L2; the counter is reset for the next launch.
-__device__ __forceinline__ void finish_norm_check(double* part, unsigned* counter, double* state,
-                                                  int* flags, int init)
-{
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last || threadIdx.x >= 32) return;
-    double v = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) v += __ldcg(part + i);
-    v = warp_sum(v);
-    if (threadIdx.x == 0) {
-        const double res = sqrt(v);
-        if (!init && res > 10.0 * state[0]) atomicOr(flags, kErrMgDiverged);
-        state[0] = res;
-        *counter = 0u;
-    }
-}
-
 __global__ void __launch_bounds__(kRedThreads) k_resid_norm_partials(Op9 A,
                                                                      const double* __restrict__ b,
                                                                      const double* __restrict__ x,

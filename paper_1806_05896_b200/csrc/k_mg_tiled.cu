@@ -70,9 +70,9 @@ __device__ __forceinline__ double prolong_at2(const double* __restrict__ ec, int
     return e;
 }
 
-template <int TX, int TY, int NS, bool VAR>
+template <int TX, int TY, int NS, bool VAR, bool RN = false>
 struct SweepShape {
-    static constexpr int H = 4 * NS;
+    static constexpr int H = 4 * NS + (RN ? 2 : 0); // RN: one more updated ring (two staged: even origin)
     static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
     static constexpr int R = RX * RY;
     // variable coefficients are staged in shared memory whenever the 11 planes
@@ -83,15 +83,26 @@ struct SweepShape {
     static constexpr size_t smem = (size_t)PLANES * R * sizeof(double);
 };
 
-template <int TX, int TY, int NS, bool VAR>
+// RN: the last sweeps of a V-cycle also run MgHierarchy::solve's divergence
+// check (multigrid.cpp:141-157): the final pass updates one ring beyond the
+// tile, so the tile's residual b - A x is exact in shared memory; its squares
+// are summed per CTA and the last CTA applies finish_norm_check.
+struct NormCheck {
+    double* part;
+    unsigned* counter;
+    double* state;
+    int* flags;
+};
+
+template <int TX, int TY, int NS, bool VAR, bool RN = false>
 __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__ b,
                                                const double* __restrict__ inv,
                                                const double* __restrict__ xin,
                                                double* __restrict__ xout,
                                                const double* __restrict__ ec, int forward,
-                                               int zero_init)
+                                               int zero_init, NormCheck nc)
 {
-    using S = SweepShape<TX, TY, NS, VAR>;
+    using S = SweepShape<TX, TY, NS, VAR, RN>;
     constexpr int H = S::H, RX = S::RX, RY = S::RY, R = S::R;
     constexpr int P = 4 * NS;
     extern __shared__ double sm[];
@@ -174,7 +185,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         const int pc = q & 3;
         const int c = forward ? pc : 3 - pc;
         const int cx = c & 1, cy = c >> 1;
-        const int g = P - 1 - q;
+        const int g = P - 1 - q + (RN ? 1 : 0);
         const int lox = max(tx0 - g, 0), hix = min(tx0 + TX + g, nx);
         const int loy = max(ty0 - g, 0), hiy = min(ty0 + TY + g, nx);
         const int lc = cy * RX + cx;
@@ -202,13 +213,34 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         __syncthreads();
     }
 
+    double acc = 0.0;
     for (int ly = ty; ly < TY; ly += 8) {
         const int gy = ty0 + ly;
         if (gy >= nx) break;
         for (int lx = tx; lx < TX; lx += 32) {
             const int gx = tx0 + lx;
-            if (gx < nx) xout[(long long)gy * nx + gx] = xs[(ly + H) * RX + lx + H];
+            if (gx >= nx) continue;
+            const int l = (ly + H) * RX + lx + H;
+            const long long i = (long long)gy * nx + gx;
+            xout[i] = xs[l];
+            if (RN) { // r = b - A x in the reference's row order (op_apply_at)
+                double sum = 0.0;
+#pragma unroll
+                for (int d = 0; d < 9; ++d) {
+                    double a = VAR ? __ldg(A.coef + cpo[d] + i) : A.c[d];
+                    if (d == 4 && A.diag) a += __ldg(A.diag + i);
+                    sum += a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
+                }
+                const double r = bs[l] - sum;
+                acc += r * r;
+            }
         }
+    }
+    if (RN) {
+        __shared__ double red[32];
+        acc = block_sum(acc, red);
+        if (threadIdx.x == 0) nc.part[blockIdx.y * gridDim.x + blockIdx.x] = acc;
+        finish_norm_check(nc.part, nc.counter, nc.state, nc.flags, 0);
     }
 }
 
@@ -328,45 +360,61 @@ __global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long 
     inv[bt * n + i] = 1.0 / a;
 }
 
-template <int TX, int TY, int NS, bool VAR>
-void sweep_go(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
-              double* xo, bool forward, bool zero_init, const double* ec)
+template <int TX, int TY, int NS, bool VAR, bool RN>
+void sweep_go_rn(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
+                 double* xo, bool forward, bool zero_init, const double* ec, const NormCheck& nc)
 {
-    constexpr size_t smem = SweepShape<TX, TY, NS, VAR>::smem;
+    constexpr size_t smem = SweepShape<TX, TY, NS, VAR, RN>::smem;
     static const bool attr = [] { // thread-safe one-time setup
-        cudaFuncSetAttribute(k_sweep<TX, TY, NS, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_sweep<TX, TY, NS, VAR, RN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         return true;
     }();
     (void)attr;
     dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
     note_launch();
-    k_sweep<TX, TY, NS, VAR><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
-                                                      zero_init ? 1 : 0);
+    k_sweep<TX, TY, NS, VAR, RN><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
+                                                          zero_init ? 1 : 0, nc);
+}
+
+// the norm-check variant only for the 1- and 2-sweep launches that end a cycle
+template <int TX, int TY, int NS, bool VAR>
+void sweep_go(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
+              double* xo, bool forward, bool zero_init, const double* ec, const NormCheck* nc)
+{
+    if constexpr (NS <= 2) {
+        if (nc) {
+            sweep_go_rn<TX, TY, NS, VAR, true>(s, A, b, inv, x, xo, forward, zero_init, ec, *nc);
+            return;
+        }
+    }
+    sweep_go_rn<TX, TY, NS, VAR, false>(s, A, b, inv, x, xo, forward, zero_init, ec, NormCheck{});
 }
 
 template <int TX, int TY, int NS>
 void sweep_pick_var(cudaStream_t s, const Op9& A, const double* b, const double* inv,
-                    const double* x, double* xo, bool forward, bool zero_init, const double* ec)
+                    const double* x, double* xo, bool forward, bool zero_init, const double* ec,
+                    const NormCheck* nc)
 {
-    if (A.coef) sweep_go<TX, TY, NS, true>(s, A, b, inv, x, xo, forward, zero_init, ec);
-    else sweep_go<TX, TY, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec);
+    if (A.coef) sweep_go<TX, TY, NS, true>(s, A, b, inv, x, xo, forward, zero_init, ec, nc);
+    else sweep_go<TX, TY, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec, nc);
 }
 
 template <int NS>
 void sweep_tile(int id, cudaStream_t s, const Op9& A, const double* b, const double* inv,
-                const double* x, double* xo, bool forward, bool zero_init, const double* ec)
+                const double* x, double* xo, bool forward, bool zero_init, const double* ec,
+                const NormCheck* nc)
 {
     switch (id) {
     case 0:
         if constexpr (NS <= 2) {
-            sweep_go<64, 32, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec);
+            sweep_go<64, 32, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec, nc);
             break;
         }
         [[fallthrough]];
-    case 1: sweep_pick_var<32, 32, NS>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    case 2: sweep_pick_var<32, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    default: sweep_pick_var<16, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    case 1: sweep_pick_var<32, 32, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc); break;
+    case 2: sweep_pick_var<32, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc); break;
+    default: sweep_pick_var<16, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc); break;
     }
 }
 
@@ -378,6 +426,7 @@ std::atomic<int> g_sweep_tile{-1}; // tuning override: -1 auto, else tile id (se
 std::atomic<int> g_sweep_fuse{2};  // sweeps fused per launch (measured best, profiles/r01/tuning.md)
 
 std::atomic<int> g_colour_split{1};
+std::atomic<int> g_fuse_norm{1};
 
 void launch_colour_split(cudaStream_t s, int nx, const double* coef, double* out)
 {
@@ -394,9 +443,10 @@ void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long 
     k_inv_diag<<<dim3((unsigned)((n + 255) / 256), batch), 256, 0, s>>>(A, inv, fcs, fds);
 }
 
-void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
+bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                         const double* x, double* xo, bool forward, bool zero_init,
-                        const double* ec, int ns)
+                        const double* ec, int ns, double* part, unsigned* counter, double* state,
+                        int* flags)
 {
     int id = g_sweep_tile;
     if (id < 0) {
@@ -409,13 +459,21 @@ void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const dou
         else id = (shared && A.coef) ? 1 : 3;
     }
     if (id == 0 && (A.coef || ns > 2)) id = 1; // 64x32 tiles: constant stencils, <= 2 sweeps
+    // fuse the divergence check when asked for, the launch sweeps <= 2 times and
+    // its grid fits the partials buffer (kNormBlocks)
+    const int T = id == 0 ? 64 : 32, TYy = id == 0 ? 32 : (id == 1 ? 32 : (id == 2 ? 16 : 16));
+    const int TXx = id == 3 ? 16 : T;
+    const long long nb = (long long)((A.nx + TXx - 1) / TXx) * ((A.nx + TYy - 1) / TYy);
+    NormCheck nc{part, counter, state, flags};
+    const NormCheck* pnc = (part && ns <= 2 && nb <= kNormBlocks) ? &nc : nullptr;
     switch (ns) {
-    case 1: sweep_tile<1>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    case 2: sweep_tile<2>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    case 3: sweep_tile<3>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    case 4: sweep_tile<4>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
-    default: sweep_tile<5>(id, s, A, b, inv, x, xo, forward, zero_init, ec); break;
+    case 1: sweep_tile<1>(id, s, A, b, inv, x, xo, forward, zero_init, ec, pnc); break;
+    case 2: sweep_tile<2>(id, s, A, b, inv, x, xo, forward, zero_init, ec, pnc); break;
+    case 3: sweep_tile<3>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr); break;
+    case 4: sweep_tile<4>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr); break;
+    default: sweep_tile<5>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr); break;
     }
+    return pnc != nullptr;
 }
 
 void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, const double* x,

@@ -42,9 +42,13 @@ extern std::atomic<int> g_cluster_bottom; // 1: levels <= 7 in the cluster kerne
 extern std::atomic<int> g_sweep_fuse;     // sweeps per launch in the V-cycle (1..5, temporal blocking)
 extern std::atomic<int> g_cluster_top8;   // 1: constant-stencil level-8 hierarchies run whole in the cluster kernel
 // inv = 1 / diag(A) precomputed per level (launch_inv_diag).
-void launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
+// With part != nullptr the launch also runs the divergence check of
+// launch_residual_norm_check on its result when it can (<= 2 sweeps, grid <=
+// kNormBlocks); returns whether it did.
+bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                         const double* x, double* xo, bool forward, bool zero_init,
-                        const double* ec, int ns);
+                        const double* ec, int ns, double* part = nullptr,
+                        unsigned* counter = nullptr, double* state = nullptr, int* flags = nullptr);
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
                      long long fds);
 // colour-split copy (Op9::csplit) of a variable operator's 8 off-diagonal planes
@@ -151,6 +155,7 @@ struct ChebWork {
 void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const double* e,
                       int steps, const ChebWork& w, double* out);
 extern std::atomic<int> g_cheb_block; // 1: up to 5 Chebyshev steps per launch (temporal blocking)
+extern std::atomic<int> g_fuse_norm;  // 1: a V-cycle's last sweep launch runs the divergence check
 
 // 2x2 control block inverse (precond.cpp:37-53, 148-157; heat timedep.cpp:383-393)
 void launch_control_2x2(cudaStream_t s, const ProbDev& P, const double* tw, const double* tv,

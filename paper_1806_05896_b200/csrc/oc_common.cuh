@@ -151,4 +151,30 @@ enum ErrFlag : int {
     kErrStateBounds = 1 << 16,    // ControlProblem::validate: y_a <= 0 <= y_b
 };
 
+// The block that completes last sums the partials (fixed order) and applies
+// the divergence check of MgHierarchy::solve (multigrid.cpp:141-157):
+// res = sqrt(sum); flag if res > 10 state[0] (unless init); state[0] = res.
+// Every block fences its partial before counting, the last one reads them
+// through L2; the counter is reset for the next launch.
+__device__ __forceinline__ void finish_norm_check(double* part, unsigned* counter, double* state,
+                                                  int* flags, int init)
+{
+    __shared__ bool last;
+    const unsigned nb = gridDim.x * gridDim.y; // partials part[blockIdx.y * gridDim.x + blockIdx.x]
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == nb - 1;
+    __syncthreads();
+    if (!last || threadIdx.x >= 32) return;
+    double v = 0.0;
+    for (int i = threadIdx.x; i < (int)nb; i += 32) v += __ldcg(part + i);
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+        const double res = sqrt(v);
+        if (!init && res > 10.0 * state[0]) atomicOr(flags, kErrMgDiverged);
+        state[0] = res;
+        *counter = 0u;
+    }
+}
+
 } // namespace ocb

@@ -352,7 +352,7 @@ BottomArgs Hierarchy::bottom_args(int kfrom, int bt) const
 }
 
 void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_in,
-                       const MgParams& p, int bt, int* flags)
+                       const MgParams& p, int bt, int* flags, bool* fused_norm)
 {
     if (k == kb_) {
         if (cluster_)
@@ -421,11 +421,16 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
         const int ns = std::min(F, p.post - done);
         ++s;
         double* out = outbuf(s);
+        // the last launch of the cycle also runs the divergence check if asked
+        const bool fuse = fused_norm && done + ns == p.post;
         {
             // the first post launch also applies the prolongation (fused)
-            ProfScope ps(c, (k == 0 && done > 0 && ns == F) ? kProfSweep : kProfCats);
-            launch_sweep_tiled(c.stream, A, b, inv_at(k, bt), cur, out, false, false,
-                               done == 0 ? ec : nullptr, ns);
+            ProfScope ps(c, (k == 0 && done > 0 && ns == F && !fuse) ? kProfSweep : kProfCats);
+            const bool f = launch_sweep_tiled(c.stream, A, b, inv_at(k, bt), cur, out, false, false,
+                                              done == 0 ? ec : nullptr, ns,
+                                              fuse ? part_.get() : nullptr, cnt_.get(),
+                                              state_.get(), flags);
+            if (fuse) *fused_norm = f;
         }
         cur = out;
         done += ns;
@@ -453,8 +458,10 @@ void Hierarchy::solve(Ctx& c, const double* b, double* x, const MgParams& p, int
     launch_norm_init(c.stream, b, n, part_.get(), cnt_.get(), state_.get());
     const Op9 A = level_op(0, bt);
     for (int cyc = 0; cyc < p.cycles; ++cyc) {
-        vcycle(c, 0, b, x, cyc == 0, p, bt, flags);
-        launch_residual_norm_check(c.stream, A, b, x, part_.get(), cnt_.get(), state_.get(), flags);
+        bool fused = false; // divergence check run by the cycle's last sweep launch
+        vcycle(c, 0, b, x, cyc == 0, p, bt, flags, g_fuse_norm.load() ? &fused : nullptr);
+        if (!fused)
+            launch_residual_norm_check(c.stream, A, b, x, part_.get(), cnt_.get(), state_.get(), flags);
     }
     launch_check("multigrid solve");
 }

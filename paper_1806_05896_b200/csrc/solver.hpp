@@ -172,7 +172,7 @@ public:
 
 private:
     void vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_in, const MgParams& p,
-                int bt, int* flags);
+                int bt, int* flags, bool* fused_norm = nullptr);
     BottomArgs bottom_args(int kfrom, int bt) const;
     void build_inv(Ctx& c);
     void build_split(Ctx& c);

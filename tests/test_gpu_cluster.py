@@ -126,3 +126,27 @@ def test_blocked_chebyshev_equals_stepwise(oc, ctx, lib, pde):
     finally:
         _tune(lib, b"cheb_block", 1)
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_divergence_check_raises_with_and_without_fusion(oc, ctx, lib, fuse):
+    """MgHierarchy::solve's residual-growth check (multigrid.cpp:141-157) on a
+    tiled fine level, run by the cycle's last sweep launch (fuse_norm=1) or by
+    its own launch (0): an indefinite operator without diagonal dominance
+    (the Poisson stencil with centre -1: Gauss-Seidel diverges) raises the
+    reference's runtime_error; a definite one does not."""
+    from paper_1806_05896_b200 import _lib
+
+    ell = 9
+    b = np.random.default_rng(3).uniform(-1, 1, ((1 << ell) - 1) ** 2)
+    try:
+        _tune(lib, b"fuse_norm", fuse)
+        good = oc.assemble9("poisson", ell)
+        good[4] += 1.0
+        oc.MgHierarchy(good, ell, ctx=ctx).solve(b, 3, 5, 5)
+        bad = oc.assemble9("poisson", ell)
+        bad[4] = -1.0
+        with pytest.raises(_lib.OptconError, match="residual growth"):
+            oc.MgHierarchy(bad, ell, ctx=ctx).solve(b, 3, 5, 5)
+    finally:
+        _tune(lib, b"fuse_norm", 1)
