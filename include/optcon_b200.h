@@ -208,8 +208,9 @@ int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
  * level-8 hierarchies, e.g. heat time blocks, solved whole in the cluster
  * kernel), "colour_split" (1: variable levels >= 511^2 sweep from a
  * colour-split coefficient copy), "cheb_block" (1: 5 Chebyshev steps per launch),
- * "fuse_norm" (1: a V-cycle's last sweep launch runs the divergence check). Only launch shapes or layouts differ; results
- * agree to rounding ("cluster_top8", "colour_split", "cheb_block", "fuse_norm" bit for bit). */
+ * "fuse_norm" (1: a V-cycle's last sweep launch runs the divergence check),
+ * "fuse_restrict" (1: a level's last pre-smoothing launch restricts its residual). Only launch shapes or layouts differ; results
+ * agree to rounding (the last five bit for bit). */
 int oc_set_tuning(const char* name, int value);
 int oc_get_tuning(const char* name, int* value);
 

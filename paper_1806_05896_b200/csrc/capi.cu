@@ -409,6 +409,7 @@ int oc_set_tuning(const char* name, int value)
         else if (k == "colour_split") ocb::g_colour_split = value;
         else if (k == "cheb_block") ocb::g_cheb_block = value;
         else if (k == "fuse_norm") ocb::g_fuse_norm = value;
+        else if (k == "fuse_restrict") ocb::g_fuse_restrict = value;
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
     });
 }
@@ -426,6 +427,7 @@ int oc_get_tuning(const char* name, int* value)
         else if (k == "colour_split") *value = ocb::g_colour_split;
         else if (k == "cheb_block") *value = ocb::g_cheb_block;
         else if (k == "fuse_norm") *value = ocb::g_fuse_norm;
+        else if (k == "fuse_restrict") *value = ocb::g_fuse_restrict;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);
     });
 }

@@ -70,9 +70,12 @@ __device__ __forceinline__ double prolong_at2(const double* __restrict__ ec, int
     return e;
 }
 
-template <int TX, int TY, int NS, bool VAR, bool RN = false>
+// MODE 0: plain; 1: + divergence check (one more updated ring); 2: + residual
+// and restriction (two more updated rings). Extra rings are staged in pairs so
+// the region origin stays even.
+template <int TX, int TY, int NS, bool VAR, int MODE = 0>
 struct SweepShape {
-    static constexpr int H = 4 * NS + (RN ? 2 : 0); // RN: one more updated ring (two staged: even origin)
+    static constexpr int H = 4 * NS + (MODE ? 2 : 0);
     static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
     static constexpr int R = RX * RY;
     // variable coefficients are staged in shared memory whenever the 11 planes
@@ -80,7 +83,8 @@ struct SweepShape {
     // otherwise read through L1 (colour-strided, L2-bandwidth bound)
     static constexpr bool CS = VAR && (size_t)11 * R * sizeof(double) <= 100 * 1024; // >= 2 CTAs/SM
     static constexpr int PLANES = CS ? 11 : 3; // x, b, inv (+ 8 off-diagonals)
-    static constexpr size_t smem = (size_t)PLANES * R * sizeof(double);
+    static constexpr int RSX = TX + 1, RSN = (TX + 1) * (TY + 1); // MODE 2: fine residual rows
+    static constexpr size_t smem = ((size_t)PLANES * R + (MODE == 2 ? RSN : 0)) * sizeof(double);
 };
 
 // RN: the last sweeps of a V-cycle also run MgHierarchy::solve's divergence
@@ -93,16 +97,24 @@ struct NormCheck {
     double* state;
     int* flags;
 };
+// MODE 2: the last pre-smoothing launch of a level also computes bc = R (b - A x)
+// for the coarse nodes whose centre fine node lies in its tile (zeroing xc),
+// as k_resid_restrict does: the final pass updates two rings beyond the tile.
+struct RestrictOut {
+    double* bc;
+    double* xc;
+};
 
-template <int TX, int TY, int NS, bool VAR, bool RN = false>
+template <int TX, int TY, int NS, bool VAR, int MODE = 0>
 __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__ b,
                                                const double* __restrict__ inv,
                                                const double* __restrict__ xin,
                                                double* __restrict__ xout,
                                                const double* __restrict__ ec, int forward,
-                                               int zero_init, NormCheck nc)
+                                               int zero_init, NormCheck nc, RestrictOut ro)
 {
-    using S = SweepShape<TX, TY, NS, VAR, RN>;
+    constexpr bool RN = MODE == 1, RR = MODE == 2;
+    using S = SweepShape<TX, TY, NS, VAR, MODE>;
     constexpr int H = S::H, RX = S::RX, RY = S::RY, R = S::R;
     constexpr int P = 4 * NS;
     extern __shared__ double sm[];
@@ -185,7 +197,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         const int pc = q & 3;
         const int c = forward ? pc : 3 - pc;
         const int cx = c & 1, cy = c >> 1;
-        const int g = P - 1 - q + (RN ? 1 : 0);
+        const int g = P - 1 - q + (RN ? 1 : 0) + (RR ? 2 : 0);
         const int lox = max(tx0 - g, 0), hix = min(tx0 + TX + g, nx);
         const int loy = max(ty0 - g, 0), hiy = min(ty0 + TY + g, nx);
         const int lc = cy * RX + cx;
@@ -241,6 +253,53 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         acc = block_sum(acc, red);
         if (threadIdx.x == 0) nc.part[blockIdx.y * gridDim.x + blockIdx.x] = acc;
         finish_norm_check(nc.part, nc.counter, nc.state, nc.flags, 0);
+    }
+    if (RR) {
+        // fine residual on [tx0, tx0+TX] x [ty0, ty0+TY] (multigrid.cpp:120-121,
+        // k_resid_restrict's order), then R = P^T for this tile's coarse nodes
+        double* rs = sm + S::PLANES * R;
+        for (int ly = ty; ly <= TY; ly += 8) {
+            const int gy = ty0 + ly;
+            for (int lx = tx; lx <= TX; lx += 32) {
+                const int gx = tx0 + lx;
+                double r = 0.0;
+                if (gx < nx && gy < nx) {
+                    const int l = (ly + H) * RX + lx + H;
+                    const long long i = (long long)gy * nx + gx;
+                    double sum = 0.0;
+#pragma unroll
+                    for (int d = 0; d < 9; ++d) {
+                        double a = VAR ? __ldg(A.coef + cpo[d] + i) : A.c[d];
+                        if (d == 4 && A.diag) a += __ldg(A.diag + i);
+                        sum += a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
+                    }
+                    r = bs[l] - sum;
+                }
+                rs[ly * S::RSX + lx] = r;
+            }
+        }
+        __syncthreads();
+        const int cx0 = tx0 / 2, cy0 = ty0 / 2;
+        for (int j = ty; j < TY / 2; j += 8) {
+            const int cy = cy0 + j;
+            for (int kx = tx; kx < TX / 2; kx += 32) {
+                const int cx = cx0 + kx;
+                if (cx >= nxc || cy >= nxc) continue;
+                double sum = 0.0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const double wy = (a == 1) ? 1.0 : 0.5;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const double wx = (c == 1) ? 1.0 : 0.5;
+                        sum += (wx * wy) * rs[(2 * j + a) * S::RSX + 2 * kx + c];
+                    }
+                }
+                const long long I = (long long)cy * nxc + cx;
+                ro.bc[I] = sum;
+                if (ro.xc) ro.xc[I] = 0.0;
+            }
+        }
     }
 }
 
@@ -360,61 +419,67 @@ __global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long 
     inv[bt * n + i] = 1.0 / a;
 }
 
-template <int TX, int TY, int NS, bool VAR, bool RN>
-void sweep_go_rn(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
-                 double* xo, bool forward, bool zero_init, const double* ec, const NormCheck& nc)
+template <int TX, int TY, int NS, bool VAR, int MODE>
+void sweep_go_mode(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
+                   double* xo, bool forward, bool zero_init, const double* ec, const NormCheck& nc,
+                   const RestrictOut& ro)
 {
-    constexpr size_t smem = SweepShape<TX, TY, NS, VAR, RN>::smem;
+    constexpr size_t smem = SweepShape<TX, TY, NS, VAR, MODE>::smem;
     static const bool attr = [] { // thread-safe one-time setup
-        cudaFuncSetAttribute(k_sweep<TX, TY, NS, VAR, RN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_sweep<TX, TY, NS, VAR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         return true;
     }();
     (void)attr;
     dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
     note_launch();
-    k_sweep<TX, TY, NS, VAR, RN><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
-                                                          zero_init ? 1 : 0, nc);
+    k_sweep<TX, TY, NS, VAR, MODE><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
+                                                            zero_init ? 1 : 0, nc, ro);
 }
 
-// the norm-check variant only for the 1- and 2-sweep launches that end a cycle
+// the fused variants only for the 1- and 2-sweep launches that end a phase
 template <int TX, int TY, int NS, bool VAR>
 void sweep_go(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
-              double* xo, bool forward, bool zero_init, const double* ec, const NormCheck* nc)
+              double* xo, bool forward, bool zero_init, const double* ec, const NormCheck* nc,
+              const RestrictOut* ro)
 {
     if constexpr (NS <= 2) {
         if (nc) {
-            sweep_go_rn<TX, TY, NS, VAR, true>(s, A, b, inv, x, xo, forward, zero_init, ec, *nc);
+            sweep_go_mode<TX, TY, NS, VAR, 1>(s, A, b, inv, x, xo, forward, zero_init, ec, *nc, RestrictOut{});
+            return;
+        }
+        if (ro) {
+            sweep_go_mode<TX, TY, NS, VAR, 2>(s, A, b, inv, x, xo, forward, zero_init, ec, NormCheck{}, *ro);
             return;
         }
     }
-    sweep_go_rn<TX, TY, NS, VAR, false>(s, A, b, inv, x, xo, forward, zero_init, ec, NormCheck{});
+    sweep_go_mode<TX, TY, NS, VAR, 0>(s, A, b, inv, x, xo, forward, zero_init, ec, NormCheck{}, RestrictOut{});
 }
 
 template <int TX, int TY, int NS>
 void sweep_pick_var(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                     const double* x, double* xo, bool forward, bool zero_init, const double* ec,
-                    const NormCheck* nc)
+                    const NormCheck* nc, const RestrictOut* ro)
 {
-    if (A.coef) sweep_go<TX, TY, NS, true>(s, A, b, inv, x, xo, forward, zero_init, ec, nc);
-    else sweep_go<TX, TY, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec, nc);
+    if (A.coef) sweep_go<TX, TY, NS, true>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
+    else sweep_go<TX, TY, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
 }
 
 template <int NS>
 void sweep_tile(int id, cudaStream_t s, const Op9& A, const double* b, const double* inv,
                 const double* x, double* xo, bool forward, bool zero_init, const double* ec,
-                const NormCheck* nc)
+                const NormCheck* nc, const RestrictOut* ro)
 {
     switch (id) {
     case 0:
         if constexpr (NS <= 2) {
-            sweep_go<64, 32, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec, nc);
+            sweep_go<64, 32, NS, false>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
             break;
         }
         [[fallthrough]];
-    case 1: sweep_pick_var<32, 32, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc); break;
-    case 2: sweep_pick_var<32, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc); break;
-    default: sweep_pick_var<16, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc); break;
+    case 1: sweep_pick_var<32, 32, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro); break;
+    case 2: sweep_pick_var<32, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro); break;
+    default: sweep_pick_var<16, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro); break;
     }
 }
 
@@ -427,6 +492,7 @@ std::atomic<int> g_sweep_fuse{2};  // sweeps fused per launch (measured best, pr
 
 std::atomic<int> g_colour_split{1};
 std::atomic<int> g_fuse_norm{1};
+std::atomic<int> g_fuse_restrict{1};
 
 void launch_colour_split(cudaStream_t s, int nx, const double* coef, double* out)
 {
@@ -446,7 +512,7 @@ void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long 
 bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                         const double* x, double* xo, bool forward, bool zero_init,
                         const double* ec, int ns, double* part, unsigned* counter, double* state,
-                        int* flags)
+                        int* flags, double* bc, double* xc)
 {
     int id = g_sweep_tile;
     if (id < 0) {
@@ -466,14 +532,16 @@ bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const dou
     const long long nb = (long long)((A.nx + TXx - 1) / TXx) * ((A.nx + TYy - 1) / TYy);
     NormCheck nc{part, counter, state, flags};
     const NormCheck* pnc = (part && ns <= 2 && nb <= kNormBlocks) ? &nc : nullptr;
+    RestrictOut ro{bc, xc};
+    const RestrictOut* pro = (!pnc && bc && ns <= 2) ? &ro : nullptr;
     switch (ns) {
-    case 1: sweep_tile<1>(id, s, A, b, inv, x, xo, forward, zero_init, ec, pnc); break;
-    case 2: sweep_tile<2>(id, s, A, b, inv, x, xo, forward, zero_init, ec, pnc); break;
-    case 3: sweep_tile<3>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr); break;
-    case 4: sweep_tile<4>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr); break;
-    default: sweep_tile<5>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr); break;
+    case 1: sweep_tile<1>(id, s, A, b, inv, x, xo, forward, zero_init, ec, pnc, pro); break;
+    case 2: sweep_tile<2>(id, s, A, b, inv, x, xo, forward, zero_init, ec, pnc, pro); break;
+    case 3: sweep_tile<3>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr, nullptr); break;
+    case 4: sweep_tile<4>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr, nullptr); break;
+    default: sweep_tile<5>(id, s, A, b, inv, x, xo, forward, zero_init, ec, nullptr, nullptr); break;
     }
-    return pnc != nullptr;
+    return pnc != nullptr || pro != nullptr;
 }
 
 void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, const double* x,

@@ -44,11 +44,13 @@ extern std::atomic<int> g_cluster_top8;   // 1: constant-stencil level-8 hierarc
 // inv = 1 / diag(A) precomputed per level (launch_inv_diag).
 // With part != nullptr the launch also runs the divergence check of
 // launch_residual_norm_check on its result when it can (<= 2 sweeps, grid <=
-// kNormBlocks); returns whether it did.
+// kNormBlocks); with bc != nullptr it also does launch_resid_restrict_tiled's
+// work (bc = R (b - A x), xc = 0; <= 2 sweeps). Returns whether it fused.
 bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                         const double* x, double* xo, bool forward, bool zero_init,
                         const double* ec, int ns, double* part = nullptr,
-                        unsigned* counter = nullptr, double* state = nullptr, int* flags = nullptr);
+                        unsigned* counter = nullptr, double* state = nullptr, int* flags = nullptr,
+                        double* bc = nullptr, double* xc = nullptr);
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
                      long long fds);
 // colour-split copy (Op9::csplit) of a variable operator's 8 off-diagonal planes
@@ -156,6 +158,7 @@ void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const d
                       int steps, const ChebWork& w, double* out);
 extern std::atomic<int> g_cheb_block; // 1: up to 5 Chebyshev steps per launch (temporal blocking)
 extern std::atomic<int> g_fuse_norm;  // 1: a V-cycle's last sweep launch runs the divergence check
+extern std::atomic<int> g_fuse_restrict; // 1: a level's last pre-smoothing launch restricts the residual
 
 // 2x2 control block inverse (precond.cpp:37-53, 148-157; heat timedep.cpp:383-393)
 void launch_control_2x2(cudaStream_t s, const ProbDev& P, const double* tw, const double* tv,

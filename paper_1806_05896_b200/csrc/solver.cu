@@ -391,16 +391,20 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
         cur = Bbuf;
     }
     int s = 0;
+    bool restricted = false; // the last pre-smoothing launch also restricted the residual
     for (int done = 0; done < p.pre;) {
         const int ns = std::min(F, p.pre - done);
         ++s;
         double* out = outbuf(s);
+        const bool fuse = g_fuse_restrict.load() && done + ns == p.pre;
         {
             // roofline sample: fine-level launches of the full fusion depth that
             // read x and apply no prolongation (the steady-state launch)
-            ProfScope ps(c, (k == 0 && ns == F && cur != nullptr) ? kProfSweep : kProfCats);
-            launch_sweep_tiled(c.stream, A, b, inv_at(k, bt), cur, out, true, cur == nullptr,
-                               nullptr, ns);
+            ProfScope ps(c, (k == 0 && ns == F && cur != nullptr && !fuse) ? kProfSweep : kProfCats);
+            restricted = launch_sweep_tiled(c.stream, A, b, inv_at(k, bt), cur, out, true, cur == nullptr,
+                                            nullptr, ns, nullptr, nullptr, nullptr, nullptr,
+                                            fuse ? b_[k + 1].get() : nullptr, xa_[k + 1].get()) &&
+                         fuse;
         }
         cur = out;
         done += ns;
@@ -410,7 +414,7 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
         launch_fill(c.stream, out, 0.0, n);
         cur = out;
     }
-    launch_resid_restrict_tiled(c.stream, A, b, cur, b_[k + 1].get(), xa_[k + 1].get());
+    if (!restricted) launch_resid_restrict_tiled(c.stream, A, b, cur, b_[k + 1].get(), xa_[k + 1].get());
     vcycle(c, k + 1, b_[k + 1].get(), xa_[k + 1].get(), true, p, bt, flags);
     const double* ec = xa_[k + 1].get();
     if (p.post == 0) {

@@ -150,3 +150,25 @@ def test_divergence_check_raises_with_and_without_fusion(oc, ctx, lib, fuse):
             oc.MgHierarchy(bad, ell, ctx=ctx).solve(b, 3, 5, 5)
     finally:
         _tune(lib, b"fuse_norm", 1)
+
+
+@pytest.mark.parametrize("knob", [b"fuse_norm", b"fuse_restrict", b"colour_split", b"cheb_block"])
+def test_fusion_knobs_leave_solutions_bitwise_unchanged(oc, ctx, lib, knob):
+    """Each kernel fusion (divergence check or residual restriction folded into
+    the last sweep launch, colour-split coefficients, blocked Chebyshev) only
+    regroups the same arithmetic: a C2-style solve at 513^2 with the knob off
+    and on gives identical bits."""
+    from paper_1806_05896_b200 import configs
+
+    c = configs.C2_CELLS[4]
+    out = {}
+    try:
+        for v in (0, 1):
+            _tune(lib, knob, v)
+            qp = oc.QpProblem(oc.ControlProblem(pde="poisson", alpha=c.alpha, beta=c.beta, y_d=c.y_d(),
+                                                u_a=c.u_a, u_b=c.u_b), oc.Grid(c.level), ctx)
+            r = oc.ipm_solve(qp, oc.IpmParams(sigma=c.sigma, solver=c.solver))
+            out[v] = (r.u, [i.lin_iters for i in r.stats.iterations])
+    finally:
+        _tune(lib, knob, 1)
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
