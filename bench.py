@@ -388,11 +388,13 @@ def run_ours(args):
     achieved = sweep_bytes / (sweep_ms / sweep_n / 1e3) / 1e9 if sweep_n else None
     kkt_b, prec_b = bytes_model.apply_bytes("pt" if args.solver == "gmres-pt" else "pd",
                                             args.level, ny)
-    kkt_ms, kkt_n = prof["kkt"]
-    prec_ms, prec_n = prof["prec"]
-    apply_gbs = None
-    if kkt_n and prec_n:
-        apply_gbs = (kkt_b + prec_b) / ((kkt_ms / kkt_n + prec_ms / prec_n) / 1e3) / 1e9
+    # KKT + preconditioner apply as the solver runs it (preconditioner graph
+    # replayed, 20 applies on cell 0's last Newton state, CUDA events on its
+    # stream); the per-launch event pass above disables graph capture
+    kind = "pt" if args.solver == "gmres-pt" else "pd"
+    kkt_ms, prec_ms = probs[0].time_applies(kind, 20)
+    kkt_n = prec_n = 1
+    apply_gbs = (kkt_b + prec_b) / ((kkt_ms + prec_ms) / 1e3) / 1e9
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -446,7 +448,11 @@ def run_ours(args):
             "kkt_precond_apply": {"gbs": apply_gbs, "kkt_ms": kkt_ms / kkt_n if kkt_n else None,
                                   "prec_ms": prec_ms / prec_n if prec_n else None,
                                   "bytes": kkt_b + prec_b, "frac_of_peak":
-                                  (apply_gbs / peak) if apply_gbs else None},
+                                  (apply_gbs / peak) if apply_gbs else None,
+                                  "how": "oc_time_applies on cell 0's last Newton state: 20 graph-"
+                                         "replayed applies, other cells idle but their contexts "
+                                         "live (launch shapes for 9 concurrent cells; alone: "
+                                         "tools/apply_bw.py); SURVEY 8d byte model"},
         }
         print(json.dumps(line), flush=True)
     if dist:
