@@ -159,8 +159,10 @@ struct Own {
 };
 
 // The NPT nodes per colour of a thread on a multi-position slab level (the
-// level-8 top): position m is colour-sub-lattice index t + 256 m, so a warp
-// covers 32 consecutive columns of one colour row.
+// level-8 top): thread t owns column t mod WX of the NPT consecutive colour
+// rows NPT (t / WX) + m, so a warp covers 32 consecutive columns of one colour
+// row and a thread's positions m, m+1 share their in-between grid row (three
+// of the eight neighbour loads).
 template <class G>
 struct OwnM {
     static constexpr int N = G::NPT;
@@ -170,9 +172,8 @@ struct OwnM {
     {
 #pragma unroll
         for (int m = 0; m < N; ++m) {
-            const int g = threadIdx.x + kCT * m;
-            rr[m] = g / G::WX;
-            cc[m] = g - rr[m] * G::WX;
+            rr[m] = N * (threadIdx.x / G::WX) + m;
+            cc[m] = threadIdx.x % G::WX;
             q[m] = rr[m] * G::SX + cc[m];
         }
         r0 = G::RP * w;
