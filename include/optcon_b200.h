@@ -202,15 +202,16 @@ int oc_debug_cluster_probes(int enable, unsigned long long* out64);
    cluster bottom applies (row-major, batch element 0) */
 int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
 /* Tuning knobs (process-wide): "sweep_tile" (-1 auto, 0: 64x32, 1: 32x32,
- * 2: 32x16, 3: 16x16 output tiles), "sweep_fuse" (1..5 smoothing sweeps
- * per launch, default 2), "cluster_bottom" (1: levels <= 7 in the 16-CTA
- * cluster kernel, 0: single-CTA bottom) and "cluster_top8" (1: constant-stencil
- * level-8 hierarchies, e.g. heat time blocks, solved whole in the cluster
- * kernel), "colour_split" (1: variable levels >= 511^2 sweep from a
- * colour-split coefficient copy), "cheb_block" (1: 5 Chebyshev steps per launch),
+ * 2: 32x16, 3: 16x16 output tiles), "sweep_fuse" (1..5 smoothing sweeps per
+ * launch, default 2), "cluster_bottom" (1: levels <= 7 in the 16-CTA cluster
+ * kernel, 0: single-CTA bottom), "cluster_top8" (1: constant-stencil level-8
+ * hierarchies, e.g. heat time blocks, solved whole in the cluster kernel),
+ * "colour_split" (1: variable levels >= 511^2 sweep from a colour-split
+ * coefficient copy), "cheb_block" (1: 5 Chebyshev steps per launch),
  * "fuse_norm" (1: a V-cycle's last sweep launch runs the divergence check),
- * "fuse_restrict" (1: a level's last pre-smoothing launch restricts its residual). Only launch shapes or layouts differ; results
- * agree to rounding (the last five bit for bit). */
+ * "fuse_restrict" (1: a level's last pre-smoothing launch restricts its
+ * residual). Only launch shapes or layouts differ; results agree to rounding,
+ * and bit for bit for the last five. */
 int oc_set_tuning(const char* name, int value);
 int oc_get_tuning(const char* name, int* value);
 
