@@ -407,6 +407,7 @@ int oc_set_tuning(const char* name, int value)
         else if (k == "cluster_bottom") ocb::g_cluster_bottom = value;
         else if (k == "cluster_top8") ocb::g_cluster_top8 = value;
         else if (k == "colour_split") ocb::g_colour_split = value;
+        else if (k == "mgs_persistent") ocb::g_mgs_persistent = value;
         else if (k == "cheb_block") ocb::g_cheb_block = value;
         else if (k == "fuse_norm") ocb::g_fuse_norm = value;
         else if (k == "fuse_restrict") ocb::g_fuse_restrict = value;
@@ -425,6 +426,7 @@ int oc_get_tuning(const char* name, int* value)
         else if (k == "cluster_bottom") *value = ocb::g_cluster_bottom;
         else if (k == "cluster_top8") *value = ocb::g_cluster_top8;
         else if (k == "colour_split") *value = ocb::g_colour_split;
+        else if (k == "mgs_persistent") *value = ocb::g_mgs_persistent;
         else if (k == "cheb_block") *value = ocb::g_cheb_block;
         else if (k == "fuse_norm") *value = ocb::g_fuse_norm;
         else if (k == "fuse_restrict") *value = ocb::g_fuse_restrict;

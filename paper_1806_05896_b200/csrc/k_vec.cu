@@ -7,6 +7,9 @@
 // the convergence scalars once per Krylov iteration.
 #include "kernels.hpp"
 
+#include <stdexcept>
+#include <string>
+
 namespace ocb {
 
 namespace {
@@ -132,6 +135,127 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_dot(const double* __restric
     }
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) part_out[blockIdx.x] = acc;
+}
+
+// Whole modified Gram-Schmidt orthogonalisation of GMRES column j in ONE
+// persistent launch (one 1024-thread CTA per SM, co-resident by cooperative
+// launch): w stays in shared memory for all j+1 steps, so each step streams
+// only v_i and v_{i+1} instead of reading and writing w as well
+// (k_dot_partials_mgs + j+1 k_mgs_dot launches move 4 vectors per step).
+// Bitwise identical to that sequence: the kMgsBlocks "virtual blocks" keep
+// their element sets (k = b*256 + t + m*kMgsBlocks*256), each thread
+// accumulates over m in the same order, the 256-thread block sum and the
+// fixed-order partial sums are the same functions; a grid barrier replaces
+// the kernel boundary between steps. Partials alternate between pa and pb;
+// the last step's (||w||^2) land in pfinal.
+constexpr int kMgsPersistThreads = 1024;
+constexpr int kMgsPersistM = 14; // elements per virtual-block thread held on chip
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kMgsPersistThreads, 1)
+    k_mgs_persistent(const double* const* __restrict__ V, double* __restrict__ w, double* H, int ld,
+                     int j, double* pa, double* pb, double* pfinal, unsigned* bar, long long n)
+{
+    extern __shared__ double ws[]; // [local vb 0..VPB)[m][t]
+    __shared__ double sh[32];
+    __shared__ double hs;
+    constexpr int GT = 256, GROUPS = kMgsPersistThreads / GT;
+    const int vpb = kMgsBlocks / gridDim.x; // virtual blocks per CTA
+    const int g = threadIdx.x / GT, t = threadIdx.x % GT;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, gw = wid % (GT / 32);
+    const long long stride = (long long)kMgsBlocks * GT;
+
+    // stage w, then the first inner product <w, v_0> (k_dot_partials on kMgsBlocks)
+    for (int s = g; s < vpb; s += GROUPS) {
+        const int vb = blockIdx.x * vpb + s;
+        double* wl = ws + (size_t)s * kMgsPersistM * GT + t;
+        double acc = 0.0;
+        const double* v0 = V[0];
+#pragma unroll 2
+        for (int m = 0; m < kMgsPersistM; ++m) {
+            const long long k = (long long)vb * GT + t + m * stride;
+            if (k < n) {
+                const double x = w[k];
+                wl[m * GT] = x;
+                acc += x * v0[k];
+            }
+        }
+        // block_sum restricted to this virtual block's 8 warps
+        acc = warp_sum(acc);
+        __syncthreads();
+        if (lane == 0) sh[wid] = acc;
+        __syncthreads();
+        double v = (lane < GT / 32 && gw == 0) ? sh[(wid / (GT / 32)) * (GT / 32) + lane] : 0.0;
+        if (gw == 0) v = warp_sum(v);
+        if (t == 0) pa[vb] = v;
+    }
+    for (int i = 0; i <= j; ++i) {
+        double* pin = (i & 1) ? pb : pa;
+        double* pout = i == j ? pfinal : ((i & 1) ? pa : pb);
+        grid_barrier(bar, gridDim.x);
+        if (threadIdx.x < 32) {
+            // sum_partials_warp's order, through L2 (the partials change every step)
+            double s = 0.0;
+            for (int q = lane; q < kMgsBlocks; q += 32) s += __ldcg(pin + q);
+            s = warp_sum(s);
+            if (threadIdx.x == 0) {
+                hs = s;
+                if (blockIdx.x == 0) H[(long long)j * ld + i] = s;
+            }
+        }
+        __syncthreads();
+        const double h = hs;
+        const double* vi = V[i];
+        const double* vn = i < j ? V[i + 1] : nullptr;
+        for (int s = g; s < vpb; s += GROUPS) {
+            const int vb = blockIdx.x * vpb + s;
+            double* wl = ws + (size_t)s * kMgsPersistM * GT + t;
+            double acc = 0.0;
+#pragma unroll 2
+            for (int m = 0; m < kMgsPersistM; ++m) {
+                const long long k = (long long)vb * GT + t + m * stride;
+                if (k < n) {
+                    const double wn = wl[m * GT] + (-h) * vi[k];
+                    wl[m * GT] = wn;
+                    acc += wn * (vn ? vn[k] : wn);
+                }
+            }
+            acc = warp_sum(acc);
+            __syncthreads();
+            if (lane == 0) sh[wid] = acc;
+            __syncthreads();
+            double v = (lane < GT / 32 && gw == 0) ? sh[(wid / (GT / 32)) * (GT / 32) + lane] : 0.0;
+            if (gw == 0) v = warp_sum(v);
+            if (t == 0) pout[vb] = v;
+        }
+    }
+    for (int s = g; s < vpb; s += GROUPS) {
+        const int vb = blockIdx.x * vpb + s;
+        const double* wl = ws + (size_t)s * kMgsPersistM * GT + t;
+        for (int m = 0; m < kMgsPersistM; ++m) {
+            const long long k = (long long)vb * GT + t + m * stride;
+            if (k < n) w[k] = wl[m * GT];
+        }
+    }
 }
 
 __global__ void k_gmres_givens(const double* __restrict__ part, GmresDev G, int j)
@@ -336,6 +460,40 @@ void launch_dot_partials_mgs(cudaStream_t s, const double* x, const double* y, l
 {
     note_launch();
     k_dot_partials<<<kMgsBlocks, kRedThreads, 0, s>>>(x, y, n, part);
+}
+
+std::atomic<int> g_mgs_persistent{8};
+
+bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, const GmresDev& G,
+                           int j, double* pa, double* pb, unsigned* bar, long long n)
+{
+    constexpr size_t smem = (size_t)(kMgsBlocks / 148) * kMgsPersistM * 256 * sizeof(double);
+    // one CTA per SM on a 148-SM B200, all co-resident; otherwise the caller
+    // runs the launch-per-step sequence (same bits)
+    static const bool ok = [] {
+        int dev = 0, sms = 0, per_sm = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return false;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms != 148 || kMgsBlocks % sms || (kMgsBlocks / sms) % (kMgsPersistThreads / 256)) return false;
+        if (cudaFuncSetAttribute(k_mgs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return false;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_persistent, kMgsPersistThreads, smem);
+        cudaGetLastError();
+        return per_sm >= 1;
+    }();
+    if (!ok || n > (long long)kMgsPersistM * kMgsBlocks * 256) return false;
+    note_launch();
+    double* H = G.H;
+    int ld = G.ld;
+    double* pfinal = (j & 1) ? pa : pb; // the natural output slot of step j
+    void* args[] = {(void*)&V, (void*)&w, (void*)&H, (void*)&ld, (void*)&j,
+                    (void*)&pa, (void*)&pb, (void*)&pfinal, (void*)&bar, (void*)&n};
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_mgs_persistent, dim3(148),
+                                                      dim3(kMgsPersistThreads), args, smem, s);
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("k_mgs_persistent: ") + cudaGetErrorString(e));
+    return true;
 }
 
 void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j)

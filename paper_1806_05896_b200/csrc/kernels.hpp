@@ -54,6 +54,7 @@ bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const dou
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
                      long long fds);
 // colour-split copy (Op9::csplit) of a variable operator's 8 off-diagonal planes
+extern std::atomic<int> g_mgs_persistent; // GMRES columns j+1 >= this use the persistent MGS launch (0: never)
 extern std::atomic<int> g_colour_split; // 1: the fine level of >= 1023^2 hierarchies sweeps from it
 void launch_colour_split(cudaStream_t s, int nx, const double* coef, double* out);
 void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, const double* x,
@@ -234,6 +235,11 @@ void launch_mgs_dot(cudaStream_t s, const double* part_in, const GmresDev& G, in
                     const double* vi, double* w, const double* vnext, double* part_out, long long n);
 void launch_mgs_step(cudaStream_t s, const double* part, const GmresDev& G, int i, int j,
                      const double* vi, double* w, long long n);
+// the whole MGS of column j (the dot + j+1 mgs_dot launches above, same bits) in
+// one cooperative launch with w in shared memory; false = not applicable here
+// (n too large, not a 148-SM device). Step j's partials land in (j & 1) ? pa : pb.
+bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, const GmresDev& G,
+                           int j, double* pa, double* pb, unsigned* bar, long long n);
 // hnext from partials -> H(j+1, j), Givens update and back substitution for y (one thread)
 void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j);
 // scal[2] = sqrt(sum part) / bnorm

@@ -1088,6 +1088,16 @@ void Problem::ensure_krylov(size_t count)
         cuda_check(cudaMemcpyAsync(Ztab_.get(), tab.data(), tab.size() * sizeof(const double*),
                                    cudaMemcpyHostToDevice, ctx.stream),
                    "Ztab upload");
+        std::vector<const double*> vt(V_.size());
+        for (size_t i = 0; i < V_.size(); ++i) vt[i] = V_[i].get();
+        Vtab_.resize(V_.size());
+        cuda_check(cudaMemcpyAsync(Vtab_.get(), vt.data(), vt.size() * sizeof(const double*),
+                                   cudaMemcpyHostToDevice, ctx.stream),
+                   "Vtab upload");
+        if (!gbar_) {
+            gbar_.resize(2);
+            cuda_check(cudaMemsetAsync(gbar_.get(), 0, 2 * sizeof(unsigned), ctx.stream), "memset");
+        }
         ctx.sync();
     }
 }
@@ -1152,11 +1162,17 @@ oc_solve_report Problem::gmres(const oc_ipm_params& p, int kind, const double* b
             // next inner product; the last one yields ||w||^2
             double* pa = part; // part_ holds 8 kRedBlocks = 2 kMgsBlocks partials
             double* pb = part + kMgsBlocks;
-            launch_dot_partials_mgs(ctx.stream, kw_.get(), V_[0].get(), n, pa);
-            for (int i = 0; i <= j; ++i) {
-                const double* next = i < j ? V_[i + 1].get() : kw_.get();
-                launch_mgs_dot(ctx.stream, pa, G, i, j, V_[i].get(), kw_.get(), next, pb, n);
-                std::swap(pa, pb);
+            const int pmin = g_mgs_persistent.load();
+            if (pmin > 0 && j + 1 >= pmin &&
+                launch_mgs_persistent(ctx.stream, Vtab_.get(), kw_.get(), G, j, pa, pb, gbar_.get(), n)) {
+                if (!(j & 1)) pa = pb; // where step j's partials (||w||^2) landed
+            } else {
+                launch_dot_partials_mgs(ctx.stream, kw_.get(), V_[0].get(), n, pa);
+                for (int i = 0; i <= j; ++i) {
+                    const double* next = i < j ? V_[i + 1].get() : kw_.get();
+                    launch_mgs_dot(ctx.stream, pa, G, i, j, V_[i].get(), kw_.get(), next, pb, n);
+                    std::swap(pa, pb);
+                }
             }
             launch_gmres_givens(ctx.stream, pa, G, j);
             launch_scale_inv(ctx.stream, kw_.get(), scal + 1, V_[j + 1].get(), n, stop_.get());

@@ -280,7 +280,8 @@ private:
     long long hierarchy_generation() const;
     // Krylov
     std::vector<DVec> V_, Z_;
-    DevArray<const double*> Ztab_;
+    DevArray<const double*> Ztab_, Vtab_; // device tables of the Z / V basis pointers
+    DevArray<unsigned> gbar_;             // grid barrier of the persistent MGS launch
     DVec kw_, kx2_, kvec_[8];
     DVec H_, cs_, sn_, g_, yls_;
     // scalars

@@ -172,3 +172,32 @@ def test_fusion_knobs_leave_solutions_bitwise_unchanged(oc, ctx, lib, knob):
     finally:
         _tune(lib, knob, 1)
     assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+
+
+@pytest.mark.parametrize("cfg", ["C3@7", "C2"])
+def test_persistent_mgs_bitwise_equal(oc, ctx, lib, cfg):
+    """GMRES orthogonalisation in one persistent launch (w in shared memory,
+    grid barrier between steps) against the launch-per-step sequence: same
+    element-to-partial map and summation order, so identical bits — on C3's
+    long P_Pi solves (j up to 200) and C2's short P_T solves (every column)."""
+    from paper_1806_05896_b200 import configs
+
+    name, _, lvl = cfg.partition("@")
+    c = configs.C2_CELLS[4] if name == "C2" else configs.ALL[name].with_level(int(lvl))
+    kw = dict(pde=c.pde, alpha=c.alpha, beta=c.beta, y_d=c.y_d(), u_a=c.u_a, u_b=c.u_b)
+    if c.y_a is not None:
+        kw.update(y_a=c.y_a, y_b=c.y_b)
+    if c.obs is not None:
+        kw["observation"] = c.obs
+    out = {}
+    try:
+        for v in (0, 1):
+            _tune(lib, b"mgs_persistent", v)
+            qp = oc.QpProblem(oc.ControlProblem(**kw), oc.Grid(c.level), ctx)
+            r = oc.ipm_solve(qp, oc.IpmParams(sigma=c.sigma, solver=c.solver))
+            out[v] = (r.u, [i.lin_iters for i in r.stats.iterations])
+    finally:
+        _tune(lib, b"mgs_persistent", 8)
+    if name == "C3":
+        assert max(out[1][1]) > 8
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
