@@ -150,23 +150,54 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs_dot(const double* __restric
 // the last step's (||w||^2) land in pfinal.
 constexpr int kMgsPersistThreads = 1024;
 constexpr int kMgsPersistM = 14; // elements per virtual-block thread held on chip
+static_assert(kMgsPersistM % 7 == 0, "loads are batched 7 at a time");
+constexpr int kMgsSmemM = kMgsPersistM - 1; // slices of w in shared memory (the last in global)
 
+__device__ __forceinline__ double ld_l2_hint(const double* p, unsigned long long pol)
+{
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// L2 prefetch of this CTA's chunks of a basis vector (one 2 KB block per
+// virtual block and m slice; the ragged end rounds down to 16 bytes)
+__device__ __forceinline__ void prefetch_chunks(const double* v, int vb0, int vpb, long long n)
+{
+    const long long stride = (long long)kMgsBlocks * 256;
+    for (int q = threadIdx.x; q < vpb * kMgsPersistM; q += blockDim.x) {
+        const long long k = (long long)(vb0 + q / kMgsPersistM) * 256 + (q % kMgsPersistM) * stride;
+        if (k >= n) continue;
+        const unsigned bytes = (unsigned)(min(256LL, n - k) * 8) & ~15u;
+        if (bytes)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(v + k), "r"(bytes) : "memory");
+    }
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid barrier over co-resident CTAs: bar[0] arrivals, bar[1] generation.
+// Release on arrival (the CTA's writes, ordered by the bar.sync before it),
+// acquire on the generation poll.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks)
 {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == nblocks - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
+        const unsigned g = ld_acquire_gpu(bar + 1);
+        unsigned old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;\n" : "=r"(old) : "l"(bar) : "memory");
+        if (old == nblocks - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(bar) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar + 1) : "memory");
         } else {
-            while (*gen == g) {
+            while (ld_acquire_gpu(bar + 1) == g) {
             }
         }
-        __threadfence();
     }
     __syncthreads();
 }
@@ -175,7 +206,11 @@ __global__ void __launch_bounds__(kMgsPersistThreads, 1)
     k_mgs_persistent(const double* const* __restrict__ V, double* __restrict__ w, double* H, int ld,
                      int j, double* pa, double* pb, double* pfinal, unsigned* bar, long long n)
 {
-    extern __shared__ double ws[]; // [local vb 0..VPB)[m][t]
+    // dynamic: ps[kMgsBlocks] partials, then ws[local vb][m < kMgsSmemM][t]; the
+    // last m slice of w (the ragged tail) stays in global memory
+    extern __shared__ double dyn[];
+    double* ps = dyn;
+    double* ws = dyn + kMgsBlocks;
     __shared__ double sh[32];
     __shared__ double hs;
     constexpr int GT = 256, GROUPS = kMgsPersistThreads / GT;
@@ -184,10 +219,22 @@ __global__ void __launch_bounds__(kMgsPersistThreads, 1)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, gw = wid % (GT / 32);
     const long long stride = (long long)kMgsBlocks * GT;
 
+    // block_sum restricted to one virtual block's 8 warps (block_sum's order)
+    auto vb_sum = [&](double acc) {
+        acc = warp_sum(acc);
+        __syncthreads();
+        if (lane == 0) sh[wid] = acc;
+        __syncthreads();
+        double v = (lane < GT / 32 && gw == 0) ? sh[(wid / (GT / 32)) * (GT / 32) + lane] : 0.0;
+        if (gw == 0) v = warp_sum(v);
+        return v;
+    };
+
     // stage w, then the first inner product <w, v_0> (k_dot_partials on kMgsBlocks)
+    if (j >= 1) prefetch_chunks(V[1], blockIdx.x * vpb, vpb, n);
     for (int s = g; s < vpb; s += GROUPS) {
         const int vb = blockIdx.x * vpb + s;
-        double* wl = ws + (size_t)s * kMgsPersistM * GT + t;
+        double* wl = ws + (size_t)s * kMgsSmemM * GT + t;
         double acc = 0.0;
         const double* v0 = V[0];
 #pragma unroll 2
@@ -195,27 +242,28 @@ __global__ void __launch_bounds__(kMgsPersistThreads, 1)
             const long long k = (long long)vb * GT + t + m * stride;
             if (k < n) {
                 const double x = w[k];
-                wl[m * GT] = x;
+                if (m < kMgsSmemM) wl[m * GT] = x;
                 acc += x * v0[k];
             }
         }
-        // block_sum restricted to this virtual block's 8 warps
-        acc = warp_sum(acc);
-        __syncthreads();
-        if (lane == 0) sh[wid] = acc;
-        __syncthreads();
-        double v = (lane < GT / 32 && gw == 0) ? sh[(wid / (GT / 32)) * (GT / 32) + lane] : 0.0;
-        if (gw == 0) v = warp_sum(v);
+        const double v = vb_sum(acc);
         if (t == 0) pa[vb] = v;
     }
     for (int i = 0; i <= j; ++i) {
         double* pin = (i & 1) ? pb : pa;
         double* pout = i == j ? pfinal : ((i & 1) ? pa : pb);
+        // the step after this one streams v_{i+2}: start it towards L2 now (the
+        // basis vectors do not depend on the reductions)
+        if (i + 2 <= j) prefetch_chunks(V[i + 2], blockIdx.x * vpb, vpb, n);
         grid_barrier(bar, gridDim.x);
+        // the partials through L2 into shared memory (one round trip), then
+        // sum_partials_warp's order from there
+        for (int q = threadIdx.x; q < kMgsBlocks; q += kMgsPersistThreads) ps[q] = __ldcg(pin + q);
+        __syncthreads();
         if (threadIdx.x < 32) {
-            // sum_partials_warp's order, through L2 (the partials change every step)
             double s = 0.0;
-            for (int q = lane; q < kMgsBlocks; q += 32) s += __ldcg(pin + q);
+#pragma unroll 8
+            for (int q = lane; q < kMgsBlocks; q += 32) s += ps[q];
             s = warp_sum(s);
             if (threadIdx.x == 0) {
                 hs = s;
@@ -224,34 +272,48 @@ __global__ void __launch_bounds__(kMgsPersistThreads, 1)
         }
         __syncthreads();
         const double h = hs;
-        const double* vi = V[i];
-        const double* vn = i < j ? V[i + 1] : nullptr;
+        // v_{i+1} is read again as v_i by the next step: keep it in L2, let v_i go
+        unsigned long long pol_first, pol_last;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_first));
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_last));
+        const double* __restrict__ vi = V[i];
+        const double* __restrict__ vn = i < j ? V[i + 1] : nullptr;
         for (int s = g; s < vpb; s += GROUPS) {
             const int vb = blockIdx.x * vpb + s;
-            double* wl = ws + (size_t)s * kMgsPersistM * GT + t;
+            double* wl = ws + (size_t)s * kMgsSmemM * GT + t;
             double acc = 0.0;
-#pragma unroll 2
-            for (int m = 0; m < kMgsPersistM; ++m) {
-                const long long k = (long long)vb * GT + t + m * stride;
-                if (k < n) {
-                    const double wn = wl[m * GT] + (-h) * vi[k];
-                    wl[m * GT] = wn;
-                    acc += wn * (vn ? vn[k] : wn);
+            // valid elements form a prefix m < mc; loads of 7 elements are issued
+            // before their updates (the order of acc is unchanged)
+            const long long k0 = (long long)vb * GT + t;
+            const int mc = k0 < n ? (int)min((long long)kMgsPersistM, (n - 1 - k0) / stride + 1) : 0;
+#pragma unroll
+            for (int m0 = 0; m0 < kMgsPersistM; m0 += 7) {
+                double a[7], c[7];
+#pragma unroll
+                for (int u = 0; u < 7; ++u) {
+                    const long long k = k0 + (m0 + u) * stride;
+                    a[u] = m0 + u < mc ? ld_l2_hint(vi + k, pol_first) : 0.0;
+                    c[u] = (vn && m0 + u < mc) ? ld_l2_hint(vn + k, pol_last) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 7; ++u) {
+                    const int m = m0 + u;
+                    if (m < mc) {
+                        double* wp = m < kMgsSmemM ? wl + m * GT : w + (k0 + m * stride);
+                        const double wn = *wp + (-h) * a[u];
+                        *wp = wn;
+                        acc += wn * (vn ? c[u] : wn);
+                    }
                 }
             }
-            acc = warp_sum(acc);
-            __syncthreads();
-            if (lane == 0) sh[wid] = acc;
-            __syncthreads();
-            double v = (lane < GT / 32 && gw == 0) ? sh[(wid / (GT / 32)) * (GT / 32) + lane] : 0.0;
-            if (gw == 0) v = warp_sum(v);
+            const double v = vb_sum(acc);
             if (t == 0) pout[vb] = v;
         }
     }
     for (int s = g; s < vpb; s += GROUPS) {
         const int vb = blockIdx.x * vpb + s;
-        const double* wl = ws + (size_t)s * kMgsPersistM * GT + t;
-        for (int m = 0; m < kMgsPersistM; ++m) {
+        const double* wl = ws + (size_t)s * kMgsSmemM * GT + t;
+        for (int m = 0; m < kMgsSmemM; ++m) {
             const long long k = (long long)vb * GT + t + m * stride;
             if (k < n) w[k] = wl[m * GT];
         }
@@ -467,7 +529,7 @@ std::atomic<int> g_mgs_persistent{8};
 bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, const GmresDev& G,
                            int j, double* pa, double* pb, unsigned* bar, long long n)
 {
-    constexpr size_t smem = (size_t)(kMgsBlocks / 148) * kMgsPersistM * 256 * sizeof(double);
+    constexpr size_t smem = ((size_t)(kMgsBlocks / 148) * kMgsSmemM * 256 + kMgsBlocks) * sizeof(double);
     // one CTA per SM on a 148-SM B200, all co-resident; otherwise the caller
     // runs the launch-per-step sequence (same bits)
     static const bool ok = [] {
