@@ -14,7 +14,9 @@ Names, argument meaning and error behaviour follow the reference C++ headers
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -59,6 +61,27 @@ class _Arg:
         return C.c_void_p(arr.ctypes.data)
 
 
+# Device objects still alive at interpreter exit are closed before module
+# teardown (problems and hierarchies before their contexts): left to the
+# finaliser, a context could otherwise be destroyed after the CUDA runtime.
+_live_objects: "weakref.WeakSet" = weakref.WeakSet()
+_live_contexts: "weakref.WeakSet" = weakref.WeakSet()
+
+
+@atexit.register
+def _close_live_objects():
+    for o in list(_live_objects):
+        try:
+            o.close()
+        except Exception:
+            pass
+    for c in list(_live_contexts):
+        try:
+            c.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One device context (CUDA stream + pinned scalars) per host thread."""
 
@@ -68,6 +91,7 @@ class Context:
         _lib.check(self._L.oc_create(C.byref(h), device))
         self.h = h
         self.device = device
+        _live_contexts.add(self)
 
     def synchronize(self):
         _lib.check(self._L.oc_synchronize(self.h))
@@ -319,6 +343,7 @@ class QpProblem:
         h = C.c_void_p()
         _lib.check(self._L.oc_problem_create(self.ctx.h, C.byref(d), C.byref(h)))
         self.h = h
+        _live_objects.add(self)
         info = _lib.ProblemInfoC()
         _lib.check(self._L.oc_problem_info_get(self.h, C.byref(info)))
         self.n, self.nt, self.ny = info.n, info.nt, info.ny
@@ -511,12 +536,16 @@ class MgHierarchy:
                                         rediscretize, C.c_double(eps), smoother_id(smoother),
                                         C.byref(h)))
         self.h = h
+        _live_objects.add(self)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.oc_mg_destroy(self.h)
+            self.h = None
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
-                self._L.oc_mg_destroy(self.h)
-                self.h = None
+            self.close()
         except Exception:
             pass
 
