@@ -210,8 +210,10 @@ int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
  * coefficient copy), "cheb_block" (1: 5 Chebyshev steps per launch),
  * "fuse_norm" (1: a V-cycle's last sweep launch runs the divergence check),
  * "fuse_restrict" (1: a level's last pre-smoothing launch restricts its
- * residual). Only launch shapes or layouts differ; results agree to rounding,
- * and bit for bit for the last five. */
+ * residual), "mgs_persistent" (GMRES columns with j+1 >= value run their
+ * modified Gram-Schmidt in one cooperative launch; default 8, 0 never).
+ * Only launch shapes or layouts differ; results agree to rounding, and bit
+ * for bit for the last six. */
 int oc_set_tuning(const char* name, int value);
 int oc_get_tuning(const char* name, int* value);
 
