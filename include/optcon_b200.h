@@ -27,7 +27,7 @@ extern "C" {
 #define OC_RUNTIME_ERROR 2
 #define OC_CUDA_ERROR 3
 
-#define OC_ABI_VERSION 1
+#define OC_ABI_VERSION 2
 
 typedef struct oc_ctx oc_ctx;         /* one per host thread / stream */
 typedef struct oc_problem oc_problem; /* device-resident QpProblem / SpaceTimeSystem */
@@ -37,10 +37,15 @@ typedef struct oc_mg oc_mg;           /* standalone multigrid hierarchy */
 enum { OC_PDE_POISSON = 0, OC_PDE_CONVDIFF = 1, OC_PDE_HEAT = 2 };
 /* SolverKind (ipm.hpp:15); OC_SOLVER_DENSE is not offered on the device */
 enum { OC_SOLVER_GMRES_PT = 0, OC_SOLVER_MINRES_PD = 1, OC_SOLVER_GMRES_PPI = 2 };
-/* smoother: 4-colour symmetric Gauss-Seidel (default, parallel), or the
- * reference's lexicographic Gauss-Seidel (multigrid.cpp:44-66) run as a
- * skewed wavefront (faithful mode) */
-enum { OC_SMOOTHER_COLOR4 = 0, OC_SMOOTHER_LEX = 1 };
+/* smoother: 4-colour symmetric Gauss-Seidel (parallel), the reference's
+ * lexicographic Gauss-Seidel (multigrid.cpp:44-66) run as a skewed wavefront
+ * (faithful mode), or AUTO (the IpmParams default): colour
+ * sweeps while every Newton solve converges; a Newton solve that stops at
+ * linear_maxit unconverged (krylov.cpp:133-212 cap: the iterate then depends
+ * on the exact preconditioner) is discarded and re-solved with the
+ * lexicographic smoother from the same Theta and right-hand side, which the
+ * rest of the IPM solve keeps. */
+enum { OC_SMOOTHER_COLOR4 = 0, OC_SMOOTHER_LEX = 1, OC_SMOOTHER_AUTO = 2 };
 /* preconditioner kinds for oc_precond_apply */
 enum { OC_PRECOND_PD = 0, OC_PRECOND_PT = 1, OC_PRECOND_PPI = 2 };
 
@@ -100,6 +105,10 @@ typedef struct {
     long long total_lin;
     double solve_ms;           /* ipm_solve device time, initial point to exit */
     double newton_ms;          /* sum of Newton-solve device times */
+    long long discarded_lin;   /* AUTO: Krylov iterations of capped colour-sweep solves
+                                  that were re-solved (in solve_ms, not in total_lin) */
+    int lex_from;              /* first Newton step (1-based) solved with the
+                                  lexicographic smoother, 0 if none */
 } oc_ipm_result;
 
 /* SolveReport (krylov.hpp:29-38) */

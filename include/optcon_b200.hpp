@@ -74,7 +74,7 @@ struct IpmParams {
     int gmres_restart = 0;
     /// OC_SMOOTHER_COLOR4 (parallel default) or OC_SMOOTHER_LEX (the
     /// reference's lexicographic Gauss-Seidel, faithful mode)
-    int smoother = OC_SMOOTHER_COLOR4;
+    int smoother = OC_SMOOTHER_AUTO;
 
     oc_ipm_params c() const
     {

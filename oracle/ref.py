@@ -96,7 +96,8 @@ def lib():
         for name in ["ref_problem_sizes", "ref_ipm_solve", "ref_kkt_apply", "ref_precond_setup",
                      "ref_precond_apply", "ref_schur_apply", "ref_time_applies", "ref_objective",
                      "ref_ipm_pieces", "ref_assemble9", "ref_mg_solve", "ref_mg_depth",
-                     "ref_mg_level_matrix", "ref_gs_sweep", "ref_cheb_apply", "ref_krylov_9diag"]:
+                     "ref_mg_level_matrix", "ref_gs_sweep", "ref_cheb_apply", "ref_krylov_9diag",
+                     "ref_newton_sample_prepare", "ref_newton_sample_run"]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -242,6 +243,24 @@ class RefProblem:
         p = params("gmres-pt", **kw)
         args = [np.ascontiguousarray(a, dtype=np.float64) for a in (theta_y, theta_w, theta_v)]
         _check(lib().ref_precond_setup(C.c_void_p(self.h), *[_ptr(a) for a in args], C.byref(p)))
+
+    def newton_sample_prepare(self, solver="gmres-pt", **kw) -> float:
+        """Form the first IPM Newton system with the reference's ipm_solve and set
+        up its preconditioner; returns the setup wall seconds."""
+        p = params(solver, **kw)
+        t = C.c_double()
+        _check(lib().ref_newton_sample_prepare(C.c_void_p(self.h), C.byref(p), C.byref(t)))
+        return t.value
+
+    def newton_sample_run(self, kind, method, maxit, tol=1e-10):
+        """The reference's gmres/minres on the prepared Newton system, at most
+        `maxit` iterations: (iterations, relative residual, wall seconds)."""
+        kinds = {"pd": 0, "pt": 1, "ppi": 2, "heat-pt": 3, "heat-pd": 4}
+        it, rr, t = C.c_int(), C.c_double(), C.c_double()
+        _check(lib().ref_newton_sample_run(C.c_void_p(self.h), kinds[kind],
+                                           {"gmres": 0, "minres": 1}[method], C.c_double(tol),
+                                           int(maxit), C.byref(it), C.byref(rr), C.byref(t)))
+        return it.value, rr.value, t.value
 
     def precond_apply(self, kind, r):
         kinds = {"pd": 0, "pt": 1, "ppi": 2, "heat-pt": 3, "heat-pd": 4}

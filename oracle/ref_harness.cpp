@@ -120,7 +120,12 @@ struct Handle {
     std::vector<ChebyshevSemiIteration> heat_cheb;
     Vector ad, bd, cd;
     std::optional<TimeSchurApprox> heat_schur;
+    // bounded Krylov sample (bench.py reference arm): first Newton system
+    Vector sample_rhs;
+    bool sample_ready = false;
 };
+
+struct CapturedNewton {}; // aborts ipm_solve after the first Newton system is formed
 
 MgOptions mg_options(const Handle& h, const ref_params& p)
 {
@@ -525,6 +530,63 @@ int ref_time_applies(void* hv, int kind, int reps, const double* x, double* kkt_
                 throw std::runtime_error(g_err);
         }
         *prec_s = (now_s() - t0) / reps;
+    });
+}
+
+int ref_newton_sample_prepare(void* hv, const ref_params* pp, double* setup_s)
+{
+    return guarded([&] {
+        Handle& h = *static_cast<Handle*>(hv);
+        IpmParams params = to_params(*pp);
+        IpmModel model = h.model;
+        ThetaBlocks theta;
+        Vector r1, r2, r3;
+        // the reference's own ipm_solve forms the first Newton system (initial
+        // point, mu <- sigma mu0, build_theta, newton_rhs: ipm.cpp:278-300)
+        model.newton_solve = [&](const ThetaBlocks& th, const Vector& a, const Vector& b,
+                                 const Vector& c, const IpmParams&) -> NewtonSolveResult {
+            theta = th;
+            r1 = a;
+            r2 = b;
+            r3 = c;
+            throw CapturedNewton{};
+        };
+        try {
+            (void)ipm_solve(model, params);
+            throw std::runtime_error("ref: ipm_solve converged before a Newton step");
+        } catch (const CapturedNewton&) {
+        }
+        if (theta.theta_y.empty()) theta.theta_y.assign(h.ny, 0.0);
+        const double t0 = now_s();
+        if (ref_precond_setup(hv, theta.theta_y.data(), theta.theta_w.data(),
+                              theta.theta_v.data(), pp) != 0)
+            throw std::runtime_error(g_err);
+        *setup_s = now_s() - t0;
+        h.theta = theta;
+        h.sample_rhs = concat(concat(r1, r2), r3);
+        h.sample_ready = true;
+    });
+}
+
+int ref_newton_sample_run(void* hv, int kind, int method, double tol, int maxit, int* iters,
+                          double* relres, double* seconds)
+{
+    return guarded([&] {
+        Handle& h = *static_cast<Handle*>(hv);
+        if (!h.sample_ready) throw std::invalid_argument("ref: newton sample not prepared");
+        const LinearOperator A = make_saddle_operator(h.model, h.theta);
+        const LinearOperator P{A.n, [&h, kind](const Vector& r, Vector& out) {
+                                   out.resize(r.size());
+                                   if (ref_precond_apply(&h, kind, r.data(), out.data()) != 0)
+                                       throw std::runtime_error(g_err);
+                               }};
+        Vector x;
+        const double t0 = now_s();
+        SolveReport rep = method == 0 ? gmres(A, P, h.sample_rhs, x, tol, maxit)
+                                      : minres(A, P, h.sample_rhs, x, tol, maxit);
+        *seconds = now_s() - t0;
+        *iters = rep.iterations;
+        *relres = rep.relative_residual;
     });
 }
 

@@ -78,6 +78,14 @@ int ref_precond_apply(void* h, int kind, const double* r, double* out);
 int ref_schur_apply(void* h, const double* r, double* out);
 /* wall seconds per KKT apply and per preconditioner apply, averaged over reps */
 int ref_time_applies(void* h, int kind, int reps, const double* x, double* kkt_s, double* prec_s);
+/* Bounded Krylov sample (bench.py's reference arm): prepare forms the first
+ * IPM Newton system through the reference's ipm_solve and sets up the
+ * preconditioner (solver as in ref_params; setup wall seconds returned); run
+ * solves it with the reference's gmres (method 0) or minres (1) for at most
+ * maxit iterations with preconditioner `kind` (ref_precond_apply kinds). */
+int ref_newton_sample_prepare(void* h, const ref_params* p, double* setup_s);
+int ref_newton_sample_run(void* h, int kind, int method, double tol, int maxit, int* iters,
+                          double* relres, double* seconds);
 /* objective of the steady QP (qp.cpp:112-121) or heat closures */
 int ref_objective(void* h, const double* y, const double* z, double* out);
 /* newton_rhs + build_theta + ipm_residuals on a given state (arrays as IpmState) */

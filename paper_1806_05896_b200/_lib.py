@@ -56,6 +56,7 @@ class IpmResultC(C.Structure):
         ("av_li", C.c_double), ("mu", C.c_double), ("objective", C.c_double),
         ("sparsity_pct", C.c_double), ("l1", C.c_double), ("nodal_sparsity_pct", C.c_double),
         ("total_lin", C.c_longlong), ("solve_ms", C.c_double), ("newton_ms", C.c_double),
+        ("discarded_lin", C.c_longlong), ("lex_from", C.c_int),
     ]
 
 

@@ -120,7 +120,7 @@ int oc_default_params(oc_ipm_params* p)
         p->mg_pre = 5;
         p->mg_post = 5;
         p->solver = OC_SOLVER_GMRES_PT;
-        p->smoother = OC_SMOOTHER_COLOR4;
+        p->smoother = OC_SMOOTHER_AUTO;
         p->gmres_restart = 0;
     });
 }

@@ -791,9 +791,11 @@ void Problem::setup_precond(int kind, const oc_ipm_params& p)
     mg_.pre = p.mg_pre;
     mg_.post = p.mg_post;
     cheb_steps_ = p.cheb_steps;
-    if (p.smoother != OC_SMOOTHER_COLOR4 && p.smoother != OC_SMOOTHER_LEX)
+    if (p.smoother != OC_SMOOTHER_COLOR4 && p.smoother != OC_SMOOTHER_LEX &&
+        p.smoother != OC_SMOOTHER_AUTO)
         throw InvalidArgument("ipm: unknown smoother");
-    smoother_ = p.smoother;
+    // (a single Newton solve outside ipm_solve has no fallback: AUTO = colour sweeps)
+    smoother_ = p.smoother == OC_SMOOTHER_LEX ? OC_SMOOTHER_LEX : OC_SMOOTHER_COLOR4;
     int* fl = flags_.get();
     const double* ty = has_sb_ ? ty_.get() : nullptr;
     if (heat_) {
@@ -899,6 +901,7 @@ void Problem::time_schur(const double* r, double* out)
         const long long off = (long long)k * ns_;
         launch_rhs_plus_mass(ctx.stream, P, r + off, k > 0 ? tf_.get() + off - ns_ : nullptr,
                              rblk_.get());
+        ProfScope ps(ctx, kProfBlock);
         Hheat_.solve(ctx, rblk_.get(), tf_.get() + off, mg_, k, fl);
     }
     launch_schur_middle(ctx.stream, P, nullptr, tf_.get(), t3_.get());
@@ -906,6 +909,7 @@ void Problem::time_schur(const double* r, double* out)
         const long long off = (long long)k * ns_;
         launch_rhs_plus_mass(ctx.stream, P, t3_.get() + off,
                              k + 1 < nt_ ? out + off + ns_ : nullptr, rblk_.get());
+        ProfScope ps(ctx, kProfBlock);
         Hheat_.solve(ctx, rblk_.get(), out + off, mg_, k, fl);
     }
 }
@@ -1399,14 +1403,27 @@ void Problem::ipm_solve(const oc_ipm_params& p, oc_ipm_result* r)
         return nrm[0] <= p.eps_p && nrm[1] <= p.eps_d && nrm[2] <= p.eps_c && state_mu <= p.eps_c;
     };
     double mu = p.mu0;
-    long long total_lin = 0;
+    long long total_lin = 0, discarded_lin = 0;
     double newton_total = 0.0;
+    // AUTO smoother: colour sweeps until a Newton solve is capped, then the
+    // lexicographic smoother from that step on (the capped solve is redone)
+    oc_ipm_params pp = p;
+    const bool autosm = p.smoother == OC_SMOOTHER_AUTO;
+    if (autosm) pp.smoother = OC_SMOOTHER_COLOR4;
+    int lex_from = p.smoother == OC_SMOOTHER_LEX ? 1 : 0;
     while (!converged() && k < p.max_iterations) {
         mu = p.sigma * mu;
         launch_theta(ctx.stream, P, S, flags_.get());
         launch_newton_rhs(ctx.stream, P, S, mu, rhs_.get());
         cudaEventRecord(ns, ctx.stream);
-        const oc_solve_report rep = newton_solve(p, rhs_.get(), sol_.get());
+        oc_solve_report rep = newton_solve(pp, rhs_.get(), sol_.get());
+        if (autosm && pp.smoother == OC_SMOOTHER_COLOR4 && !rep.converged &&
+            rep.iterations >= p.linear_maxit) {
+            discarded_lin += rep.iterations;
+            pp.smoother = OC_SMOOTHER_LEX;
+            lex_from = k + 1;
+            rep = newton_solve(pp, rhs_.get(), sol_.get());
+        }
         cudaEventRecord(ne, ctx.stream);
         launch_recover_ratios(ctx.stream, P, S, mu, part_.get());
         launch_step_lengths(ctx.stream, part_.get(), p.alpha0, steps);
@@ -1455,6 +1472,8 @@ void Problem::ipm_solve(const oc_ipm_params& p, oc_ipm_result* r)
     r->mu = state_mu;
     r->solve_ms = sms;
     r->newton_ms = newton_total;
+    r->discarded_lin = discarded_lin;
+    r->lex_from = lex_from;
     r->n_records = (int)recs.size();
     if (r->records)
         for (int i = 0; i < std::min(r->n_records, r->records_cap); ++i) r->records[i] = recs[i];

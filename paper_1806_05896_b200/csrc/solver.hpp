@@ -79,7 +79,8 @@ using DVec = DevArray<double>;
 
 // Per-launch CUDA-event spans on the solver stream for the bench's in-situ
 // kernel timing (fine-level smoothing sweeps, KKT applies, P applies).
-enum ProfCat { kProfSweep = 0, kProfKkt = 1, kProfPrec = 2, kProfNewton = 3, kProfCats = 4 };
+// kProfBlock: one heat time-block multigrid solve (the level-8 cluster launch)
+enum ProfCat { kProfSweep = 0, kProfKkt = 1, kProfPrec = 2, kProfBlock = 3, kProfCats = 4 };
 struct Profiler {
     bool on = false;
     struct Span {

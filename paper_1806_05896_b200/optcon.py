@@ -116,11 +116,11 @@ class Context:
         _lib.check(self._L.oc_profile(self.h, int(enable)))
 
     def profile_read(self):
-        """{'sweep'|'kkt'|'prec': (total_ms, count)} since the last read."""
+        """{"sweep"|"kkt"|"prec"|"block": (total_ms, count)} since the last read."""
         ms = (C.c_double * 4)()
         cnt = (C.c_longlong * 4)()
         _lib.check(self._L.oc_profile_read(self.h, ms, cnt))
-        return {k: (ms[i], cnt[i]) for i, k in enumerate(("sweep", "kkt", "prec", "newton"))}
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(("sweep", "kkt", "prec", "block"))}
 
     @staticmethod
     def launch_count() -> int:
@@ -191,11 +191,12 @@ class ControlProblem:
     observation: Optional[Sequence[float]] = None  # (a1, b1, a2, b2)
 
 
-SMOOTHERS = {"color4": 0, "lex": 1}
+SMOOTHERS = {"color4": 0, "lex": 1, "auto": 2}
 
 
 def smoother_id(s) -> int:
-    """'color4' (4-colour symmetric GS, default) or 'lex' (the reference's
+    """'auto' (default: colour sweeps, lexicographic after a capped solve), 'color4'
+    (4-colour symmetric GS) or 'lex' (the reference's
     lexicographic GS, multigrid.cpp:44-66, faithful mode); ints pass through."""
     if isinstance(s, str):
         if s not in SMOOTHERS:
@@ -222,7 +223,9 @@ class IpmParams:
     mg_pre: int = 5
     mg_post: int = 5
     solver: str = "gmres-pt"
-    smoother: object = "color4"  # or "lex"
+    # "auto" (default): colour sweeps, lexicographic from the first Newton solve
+    # capped at linear_maxit on (that solve redone); "color4"; "lex" (faithful)
+    smoother: object = "auto"
     gmres_restart: int = 0
 
     def c(self) -> _lib.IpmParamsC:
@@ -286,6 +289,8 @@ class IpmResult:
     total_lin: int
     solve_ms: float
     newton_ms: float
+    discarded_lin: int = 0  # auto smoother: iterations of capped colour solves redone
+    lex_from: int = 0       # first Newton step solved with the lexicographic smoother
 
 
 @dataclass
@@ -503,7 +508,8 @@ def ipm_solve(qp: QpProblem, params: IpmParams = IpmParams(), outputs=None) -> I
     state = IpmState(o["y"], o["z"], o["p"], o["lam_ya"], o["lam_yb"], o["lam_za"],
                      o["lam_zb"], r.mu, r.nli)
     return IpmResult(state, o["u"], SparsityReport(r.sparsity_pct, r.l1), stats, r.objective,
-                     r.nodal_sparsity_pct, r.total_lin, r.solve_ms, r.newton_ms)
+                     r.nodal_sparsity_pct, r.total_lin, r.solve_ms, r.newton_ms,
+                     r.discarded_lin, r.lex_from)
 
 
 def solve_heat_control(problem: ControlProblem, grid: Grid, params: IpmParams = IpmParams(),

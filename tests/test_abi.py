@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     for fn in header_functions():
         assert hasattr(L, fn), fn
     assert set(header_functions()) == set(_lib.EXPORTS)
-    assert L.oc_abi_version() == 1
+    assert L.oc_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_device():

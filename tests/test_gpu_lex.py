@@ -130,6 +130,34 @@ def test_capped_c3_needs_the_reference_smoother(oc, ctx):
     g = load_golden("c3_l6_capped")
     qp = qp_from_golden(oc, ctx, g)
     s = g["meta"]["solve"]
-    r = oc.ipm_solve(qp, oc.IpmParams(sigma=s["sigma"], solver=s["solver"],
+    r = oc.ipm_solve(qp, oc.IpmParams(sigma=s["sigma"], solver=s["solver"], smoother="color4",
                                       linear_maxit=s["linear_maxit"]))
     assert rel(r.u, g["u"]) > 1e-8
+
+
+def test_capped_c3_default_auto_smoother_matches_reference(oc, ctx):
+    # the default smoother ("auto") redoes the first capped Newton solve with the
+    # lexicographic smoother and keeps it: the capped fixture then matches
+    g = load_golden("c3_l6_capped")
+    qp = qp_from_golden(oc, ctx, g)
+    s = g["meta"]["solve"]
+    r = oc.ipm_solve(qp, oc.IpmParams(sigma=s["sigma"], solver=s["solver"],
+                                      linear_maxit=s["linear_maxit"]))
+    assert r.lex_from >= 1 and r.discarded_lin >= s["linear_maxit"]
+    assert rel(r.u, g["u"]) <= 1e-8, rel(r.u, g["u"])
+    assert rel(r.state.y, g["y"]) <= 1e-8
+    assert int((np.abs(r.u) < 1e-2).sum()) == int((np.abs(g["u"]) < 1e-2).sum())
+    lin_ref = [int(x) for x in g["records"][1:, 5]]
+    lin_gpu = [it.lin_iters for it in r.stats.iterations[1:]]
+    assert lin_gpu == lin_ref, (lin_gpu, lin_ref)
+
+
+def test_auto_smoother_is_colour_when_nothing_is_capped(oc, ctx):
+    # converging Newton solves never trigger the fallback: bitwise the colour path
+    g = load_golden("c1_l6_gmres")
+    qp = qp_from_golden(oc, ctx, g)
+    s = g["meta"]["solve"]
+    ra = oc.ipm_solve(qp, oc.IpmParams(sigma=s["sigma"], solver=s["solver"]))
+    rc = oc.ipm_solve(qp, oc.IpmParams(sigma=s["sigma"], solver=s["solver"], smoother="color4"))
+    assert ra.lex_from == 0 and ra.discarded_lin == 0
+    assert np.array_equal(ra.u, rc.u) and np.array_equal(ra.state.y, rc.state.y)

@@ -15,10 +15,13 @@ from paper_1806_05896_b200 import _lib, configs, optcon as oc  # noqa: E402
 
 args = sys.argv[1:]
 smoother = "color4"
+solver = None
 while args[:1] and args[0].startswith("--"):
     flag, val, args = args[0], args[1], args[2:]
     if flag == "--smoother":
         smoother = val
+    elif flag == "--solver":
+        solver = val
     elif flag == "--tune":  # name=value, any oc_set_tuning knob
         key, v = val.split("=")
         _lib.check(_lib.load().oc_set_tuning(key.encode(), int(v)))
@@ -41,7 +44,7 @@ for name in names:
     t0 = time.perf_counter()
     qp = oc.QpProblem(oc.ControlProblem(**kw), oc.Grid(c.level), ctx)
     t_setup = time.perf_counter() - t0
-    params = oc.IpmParams(sigma=c.sigma, solver=c.solver, gmres_restart=c.gmres_restart,
+    params = oc.IpmParams(sigma=c.sigma, solver=solver or c.solver, gmres_restart=c.gmres_restart,
                           smoother=smoother)
     t0 = time.perf_counter()
     try:
@@ -51,7 +54,7 @@ for name in names:
         continue
     wall = time.perf_counter() - t0
     print(json.dumps({
-        "config": name, "level": c.level, "solver": c.solver, "smoother": smoother, "setup_s": round(t_setup, 3),
+        "config": name, "level": c.level, "solver": solver or c.solver, "smoother": smoother, "setup_s": round(t_setup, 3),
         "solve_ms": round(r.solve_ms, 2), "wall_s": round(wall, 3), "nli": r.stats.nli,
         "av_li": round(r.stats.av_li, 3), "converged": r.stats.converged,
         "lin_iters": [i.lin_iters for i in r.stats.iterations[1:]],
