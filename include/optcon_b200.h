@@ -224,6 +224,11 @@ int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
  * Only launch shapes or layouts differ; results agree to rounding, and bit
  * for bit for the last six. */
 int oc_set_tuning(const char* name, int value);
+/* Test hook: the lexicographic update's quotient (RN(1/d) product plus one
+ * Markstein correction) against div.rn.f64 on n operand pairs (host or device
+ * arrays); *mismatches = number of results that differ in any bit. */
+int oc_debug_lex_div(oc_ctx* ctx, const double* num, const double* den, long long n,
+                     unsigned long long* mismatches);
 int oc_get_tuning(const char* name, int* value);
 
 /* Q1 assembly into 9 coefficient arrays (fem.cpp:142-180; what: 0 mass,

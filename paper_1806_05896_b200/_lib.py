@@ -96,7 +96,7 @@ EXPORTS = [
     "oc_mg_solve", "oc_mg_depth", "oc_mg_level_matrix", "oc_mg_destroy", "oc_mg_smooth",
     "oc_cheb_apply", "oc_assemble9", "oc_launch_count", "oc_profile", "oc_profile_read",
     "oc_event_record", "oc_event_elapsed", "oc_debug_cluster_probes", "oc_debug_coarse_op", "oc_event_elapsed_between",
-    "oc_set_tuning", "oc_get_tuning", "oc_assemble9_device",
+    "oc_set_tuning", "oc_get_tuning", "oc_assemble9_device", "oc_debug_lex_div",
 ]
 
 _lib = None
@@ -153,6 +153,7 @@ def load():
     L.oc_event_elapsed_between.argtypes = [vp, C.c_int, vp, C.c_int, _dp]
     L.oc_debug_cluster_probes.argtypes = [C.c_int, vp]
     L.oc_debug_coarse_op.argtypes = [vp, C.c_int, C.c_int, vp]
+    L.oc_debug_lex_div.argtypes = [vp, vp, vp, C.c_longlong, C.POINTER(C.c_ulonglong)]
     L.oc_set_tuning.argtypes = [C.c_char_p, C.c_int]
     L.oc_get_tuning.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
     _lib = L

@@ -447,8 +447,28 @@ int oc_debug_coarse_op(oc_mg* m, int pre, int post, double* out)
     });
 }
 
+int oc_debug_lex_div(oc_ctx* c, const double* num, const double* den, long long n,
+                     unsigned long long* mismatches)
+{
+    return guarded([&] {
+        require(c, "oc_debug_lex_div");
+        require(mismatches, "oc_debug_lex_div");
+        ocb::DVec a((size_t)n), b((size_t)n);
+        ocb::DevArray<unsigned long long> bad(1);
+        ocb::copy_any(c->ctx, a.get(), num, (size_t)n * 8);
+        ocb::copy_any(c->ctx, b.get(), den, (size_t)n * 8);
+        cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), c->ctx.stream);
+        ocb::launch_lex_div_check(c->ctx.stream, a.get(), b.get(), n, bad.get());
+        ocb::copy_any(c->ctx, mismatches, bad.get(), sizeof(unsigned long long));
+        c->ctx.sync();
+        ocb::cuda_check(cudaGetLastError(), "lex division check");
+    });
+}
+
 int oc_debug_cluster_probes(int enable, unsigned long long* out64)
 {
+    // enable >= 2: the lexicographic sweep's stamps instead (out64: 512 words)
+    if (enable >= 2) return guarded([&] { ocb::lex_probes(enable - 2, out64); });
     return guarded([&] { ocb::cluster_probes(enable, out64); });
 }
 

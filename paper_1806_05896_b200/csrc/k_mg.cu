@@ -273,7 +273,7 @@ constexpr int kBtLexR = 4;
 constexpr int kBtLexPF = 0; // L1 prefetch distance (0: off)
 
 struct BtRaw {
-    double b, e, nw, nn, ne, inv;
+    double b, e, nw, nn, ne, inv, dd;
     double a[8];
 };
 
@@ -283,6 +283,7 @@ __device__ __forceinline__ void bt_lex_load(BtRaw& p, const Op9& A, const double
                                             bool hasN, bool fwd, int col)
 {
     p.b = p.e = p.nw = p.nn = p.ne = p.inv = 0.0;
+    p.dd = 1.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) p.a[k] = 0.0;
     if (!rowok || col < 0 || col >= nx) return;
@@ -301,6 +302,7 @@ __device__ __forceinline__ void bt_lex_load(BtRaw& p, const Op9& A, const double
     }
     p.b = bsm[i];
     p.inv = ism[i];
+    p.dd = diag_at(A, i, n);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const int d = k < 4 ? k : k + 1;
@@ -347,11 +349,6 @@ __device__ void bt_sweep_lex(const Op9& A, const double* bsm, double* xsm, const
                 const int st = base + u;
                 const int xl = st - 2 * j;
                 const BtRaw& p = ring[u];
-                double t = p.b;
-                t -= p.a[4] * p.e;
-                t -= p.a[5] * p.nw;
-                t -= p.a[6] * p.nn;
-                t -= p.a[7] * p.ne;
                 double up = __shfl_up_sync(0xffffffffu, last, 1);
                 if (j == 0) {
                     const int xe = st + 1;
@@ -362,11 +359,10 @@ __device__ void bt_sweep_lex(const Op9& A, const double* bsm, double* xsm, const
                 se = up;
                 double v = 0.0;
                 if (rowok && xl >= 0 && xl < nx) {
-                    t -= p.a[0] * sw;
-                    t -= p.a[1] * s;
-                    t -= p.a[2] * se;
-                    t -= p.a[3] * last;
-                    v = t * p.inv;
+                    // the reference's update (multigrid.cpp:49-60): ascending
+                    // physical columns, separate multiply and subtract, s / a_ii
+                    v = lex_update_ref(p.a, fwd, p.b, sw, s, se, last, p.e, p.nw, p.nn, p.ne, p.dd,
+                                       p.inv);
                     xsm[row0 + xl * sx] = v;
                     if (producer) mb_out[xl] = v;
                 }

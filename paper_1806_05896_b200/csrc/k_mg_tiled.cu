@@ -408,7 +408,8 @@ __global__ void k_colour_split(int nx, const double* __restrict__ coef, double* 
     out[p * n + o] = coef[d * n + i];
 }
 
-__global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long long fds)
+__global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long long fds,
+                           double* __restrict__ dfull)
 {
     const long long n = (long long)A.nx * A.nx;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -417,6 +418,7 @@ __global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long 
     double a = A.coef ? A.coef[bt * fcs + 4 * n + i] : A.c[4];
     if (A.diag) a += A.diag[bt * fds + i];
     inv[bt * n + i] = 1.0 / a;
+    if (dfull) dfull[bt * n + i] = a;
 }
 
 template <int TX, int TY, int NS, bool VAR, int MODE>
@@ -502,11 +504,11 @@ void launch_colour_split(cudaStream_t s, int nx, const double* coef, double* out
 }
 
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
-                     long long fds)
+                     long long fds, double* dfull)
 {
     const long long n = (long long)A.nx * A.nx;
     note_launch();
-    k_inv_diag<<<dim3((unsigned)((n + 255) / 256), batch), 256, 0, s>>>(A, inv, fcs, fds);
+    k_inv_diag<<<dim3((unsigned)((n + 255) / 256), batch), 256, 0, s>>>(A, inv, fcs, fds, dfull);
 }
 
 bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const double* inv,

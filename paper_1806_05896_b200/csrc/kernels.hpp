@@ -51,8 +51,9 @@ bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const dou
                         const double* ec, int ns, double* part = nullptr,
                         unsigned* counter = nullptr, double* state = nullptr, int* flags = nullptr,
                         double* bc = nullptr, double* xc = nullptr);
+// (dfull != nullptr: also the diagonal values themselves)
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
-                     long long fds);
+                     long long fds, double* dfull = nullptr);
 // colour-split copy (Op9::csplit) of a variable operator's 8 off-diagonal planes
 extern std::atomic<int> g_mgs_persistent; // GMRES columns j+1 >= this use the persistent MGS launch (0: never)
 extern std::atomic<int> g_colour_split; // 1: the fine level of >= 1023^2 hierarchies sweeps from it
@@ -89,8 +90,12 @@ void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double*
 // k_mg_lex.cu: one lexicographic Gauss-Seidel sweep in place (the reference
 // smoother, multigrid.cpp:44-66) as a skewed wavefront; inv = 1/diag(A);
 // mbox = ceil(nx/32) * nx doubles holding kLexSentinel (restored on return).
-void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* inv, double* x,
-                   bool forward, double* mbox, int* flags);
+// dfull = a_ii (the CSR diagonal value: centre coefficient + added diagonal).
+void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* inv,
+                   const double* dfull, double* x, bool forward, double* mbox, int* flags);
+// test hook: mismatches of the lexicographic update's quotient vs div.rn.f64
+void launch_lex_div_check(cudaStream_t s, const double* num, const double* den, long long n,
+                          unsigned long long* bad);
 double lex_sentinel_host();
 
 // k_assembly.cu: Q1 assembly on the device (what: 0 mass, 1 Poisson, 2 SUPG
@@ -110,6 +115,7 @@ bool cluster_bottom_supported();
 bool cluster_top8_supported(); // the level-8 (constant stencil + diagonal) variant fits this device
 // tuning aid: enable %globaltimer phase probes; read the last launch's stamps
 void cluster_probes(int enable, unsigned long long* out64);
+void lex_probes(int enable, unsigned long long* out512); // lexicographic sweep stamps
 void launch_bottom_cluster(cudaStream_t s, const ClusterArgs& a, const double* b, double* x,
                            int cycles, int pre, int post, bool check, double* state, int* flags);
 // Dense operator of the V-cycle below level 5 (levels 4, 3 and the level-2 LU)

@@ -15,8 +15,11 @@
 // mirrored coordinates: logical (x, r) is physical (nx-1-x, nx-1-r) and
 // stencil entry d becomes 8-d.
 //
-// Summation order: old-value terms, then SW, S, SE, W, times 1/a_ii. This is
-// a reassociation of the reference's loop (rounding-level difference only).
+// Arithmetic (lex_update_ref): the reference's gauss_seidel_sweep update
+// (multigrid.cpp:49-60) term by term: s = b; s -= a_ij x_j over the row's
+// columns in ascending physical order with separate multiply and subtract
+// (multigrid.cpp is compiled without FMA contraction); x_i = s / a_ii
+// correctly rounded.
 #pragma once
 
 #include "oc_common.cuh"
@@ -35,23 +38,45 @@ __device__ __forceinline__ bool lex_is_sentinel(double v)
 
 __device__ __forceinline__ double lex_sentinel() { return __longlong_as_double((long long)kLexSentinel); }
 
-// x_new = (b - sum_{d != 4} a_d x_d) / a_ii with the old-value terms first.
-// a(d) returns the coefficient of LOGICAL stencil entry d.
-template <class Coef>
-__device__ __forceinline__ double lex_update(const Coef& a, double bval, double inv, double sw,
-                                             double s, double se, double w, double e, double nw,
-                                             double n, double ne)
+// s / d correctly rounded from inv = RN(1/d): one Markstein correction with
+// the exact FMA remainder (tested equal to div.rn.f64, tests/test_gpu_lex.py).
+__device__ __forceinline__ double lex_div_rn(double s, double d, double inv)
 {
-    double t = bval;
-    t -= a(5) * e;
-    t -= a(6) * nw;
-    t -= a(7) * n;
-    t -= a(8) * ne;
-    t -= a(0) * sw;
-    t -= a(1) * s;
-    t -= a(2) * se;
-    t -= a(3) * w;
-    return t * inv;
+    const double q0 = __dmul_rn(s, inv);
+    const double r = __fma_rn(-q0, d, s);
+    return __fma_rn(r, inv, q0);
+}
+
+// The reference's node update in logical coordinates: a[0..7] are the
+// LOGICAL entries SW,S,SE,W,E,NW,N,NE; forward sweeps subtract them in that
+// order, backward (mirrored) sweeps in the reverse order (= physical
+// ascending columns).
+__device__ __forceinline__ double lex_update_ref(const double* a, bool fwd, double b, double sw,
+                                                 double s, double se, double w, double e,
+                                                 double nw, double n, double ne, double d,
+                                                 double inv)
+{
+    double t = b;
+    if (fwd) {
+        t = __dsub_rn(t, __dmul_rn(a[0], sw));
+        t = __dsub_rn(t, __dmul_rn(a[1], s));
+        t = __dsub_rn(t, __dmul_rn(a[2], se));
+        t = __dsub_rn(t, __dmul_rn(a[3], w));
+        t = __dsub_rn(t, __dmul_rn(a[4], e));
+        t = __dsub_rn(t, __dmul_rn(a[5], nw));
+        t = __dsub_rn(t, __dmul_rn(a[6], n));
+        t = __dsub_rn(t, __dmul_rn(a[7], ne));
+    } else {
+        t = __dsub_rn(t, __dmul_rn(a[7], ne));
+        t = __dsub_rn(t, __dmul_rn(a[6], n));
+        t = __dsub_rn(t, __dmul_rn(a[5], nw));
+        t = __dsub_rn(t, __dmul_rn(a[4], e));
+        t = __dsub_rn(t, __dmul_rn(a[3], w));
+        t = __dsub_rn(t, __dmul_rn(a[2], se));
+        t = __dsub_rn(t, __dmul_rn(a[1], s));
+        t = __dsub_rn(t, __dmul_rn(a[0], sw));
+    }
+    return lex_div_rn(t, d, inv);
 }
 
 } // namespace ocb

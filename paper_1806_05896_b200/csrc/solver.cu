@@ -196,7 +196,12 @@ void Hierarchy::allocate(int level, int batch, int smoother)
     xb_[0].resize((size_t)level_n(0));
     inv_.clear();
     inv_.resize(K_ + 1);
-    for (int k = 0; k < kb_; ++k) inv_[k].resize((size_t)level_n(k) * batch);
+    dfull_.clear();
+    dfull_.resize(K_ + 1);
+    for (int k = 0; k < kb_; ++k) {
+        inv_[k].resize((size_t)level_n(k) * batch);
+        if (lex_) dfull_[k].resize((size_t)level_n(k) * batch);
+    }
     if (lex_) {
         const int nx0 = nx_[0];
         mbox_.resize((size_t)((nx0 + 31) / 32) * nx0);
@@ -303,7 +308,7 @@ void Hierarchy::build_inv(Ctx& c)
         const Op9 a = level_op(k, 0);
         const long long cs = k == 0 ? fine_coef_stride_ : 9 * level_n(k);
         const long long ds = k == 0 ? fine_diag_stride_ : 0;
-        launch_inv_diag(c.stream, a, inv_[k].get(), batch_, cs, ds);
+        launch_inv_diag(c.stream, a, inv_[k].get(), batch_, cs, ds, lex_ ? dfull_[k].get() : nullptr);
     }
     if (lex_) launch_fill(c.stream, mbox_.get(), lex_sentinel_host(), (long long)mbox_.size());
 }
@@ -368,12 +373,12 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
         // reference cycle (multigrid.cpp:111-132) with in-place lexicographic sweeps
         if (zero_in) launch_fill(c.stream, xout, 0.0, level_n(k));
         for (int s = 0; s < p.pre; ++s)
-            launch_gs_lex(c.stream, A, b, inv_at(k, bt), xout, true, mbox_.get(), flags);
+            launch_gs_lex(c.stream, A, b, inv_at(k, bt), dfull_at(k, bt), xout, true, mbox_.get(), flags);
         launch_resid_restrict_tiled(c.stream, A, b, xout, b_[k + 1].get(), xa_[k + 1].get());
         vcycle(c, k + 1, b_[k + 1].get(), xa_[k + 1].get(), true, p, bt, flags);
         launch_prolong_add(c.stream, nx_[k], xa_[k + 1].get(), xout);
         for (int s = 0; s < p.post; ++s)
-            launch_gs_lex(c.stream, A, b, inv_at(k, bt), xout, false, mbox_.get(), flags);
+            launch_gs_lex(c.stream, A, b, inv_at(k, bt), dfull_at(k, bt), xout, false, mbox_.get(), flags);
         return;
     }
     double* Abuf = xout;
@@ -473,12 +478,12 @@ void Hierarchy::solve(Ctx& c, const double* b, double* x, const MgParams& p, int
 void Hierarchy::smooth(Ctx& c, const double* b, double* x, bool forward, int bt)
 {
     const Op9 A = level_op(0, bt);
-    DVec inv((size_t)level_n(0));
-    launch_inv_diag(c.stream, A, inv.get(), 1, 0, 0);
+    DVec inv((size_t)level_n(0)), dfull((size_t)level_n(0));
+    launch_inv_diag(c.stream, A, inv.get(), 1, 0, 0, dfull.get());
     if (lex_) {
         DevArray<int> fl(1);
         cudaMemsetAsync(fl.get(), 0, sizeof(int), c.stream);
-        launch_gs_lex(c.stream, A, b, inv.get(), x, forward, mbox_.get(), fl.get());
+        launch_gs_lex(c.stream, A, b, inv.get(), dfull.get(), x, forward, mbox_.get(), fl.get());
         c.sync();
         launch_check("smoothing sweep");
         return;

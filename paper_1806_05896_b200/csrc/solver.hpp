@@ -178,6 +178,7 @@ private:
     void build_inv(Ctx& c);
     void build_split(Ctx& c);
     const double* inv_at(int k, int bt) const { return inv_[k].get() + (size_t)bt * level_n(k); }
+    const double* dfull_at(int k, int bt) const { return dfull_[k].get() + (size_t)bt * level_n(k); }
 
     int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1, smoother_ = OC_SMOOTHER_COLOR4;
     bool lex_ = false;     // lexicographic smoother: in-place wavefront sweeps, single-CTA bottom
@@ -192,6 +193,7 @@ private:
     DVec remfine_;                  // fine remainder fine - base(level), 9 arrays
     std::vector<DVec> xa_, xb_, b_; // per level work (k >= 1); xb_[0] fine scratch
     std::vector<DVec> inv_;         // 1/diag per tiled level (k < kb_), batch-strided
+    std::vector<DVec> dfull_;       // lexicographic mode: the diagonal values themselves
     DVec lu_;
     DevArray<int> perm_;
     std::vector<DVec> split_;       // [k] colour-split off-diagonals of variable tiled levels >= 511^2 (batch 1)

@@ -47,6 +47,50 @@ def test_lex_sweep_is_reference_order(oc, ctx, port, ell, kind):
         assert rel(got, want) <= 1e-12, (fwd, rel(got, want))
 
 
+@pytest.mark.parametrize("ell", [3, 6, 7, 8, 10])
+@pytest.mark.parametrize("kind", ["poisson+diag", "convdiff"])
+def test_lex_sweep_bitwise_equals_reference(oc, ctx, refmod, ell, kind):
+    # the node update follows multigrid.cpp:49-60 operation by operation
+    # (ascending columns, separate multiply and subtract, s / a_ii correctly
+    # rounded): a sweep equals the reference library's gauss_seidel_sweep
+    # bit for bit, forward and backward, on every level size (one band,
+    # several bands, 32 bands at 1023^2)
+    A = operator(oc, kind, ell, ell)
+    rng = np.random.default_rng(200 + ell)
+    b, x0 = rng.uniform(-1, 1, (2, A.shape[1]))
+    mg = oc.MgHierarchy(A, ell, ctx=ctx, smoother="lex")
+    for fwd in (True, False):
+        got = mg.smooth(b, x0, fwd)
+        want = refmod.gs_sweep(ell, A, b, x0, fwd)
+        assert np.array_equal(got, want), (fwd, rel(got, want), int((got != want).sum()))
+
+
+def test_lex_division_is_correctly_rounded(oc, ctx):
+    # the update's quotient (RN(1/d) product + one Markstein correction) equals
+    # the IEEE division on random operands over many binades and on the
+    # solver's own kind of data (diagonals of L + diag, coarse Galerkin rows)
+    import ctypes as C
+
+    from paper_1806_05896_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    n = 1 << 22
+    cases = [
+        (rng.standard_normal(n) * 10.0 ** rng.uniform(-30, 30, n),
+         rng.standard_normal(n) * 10.0 ** rng.uniform(-30, 30, n)),
+        (rng.uniform(-1, 1, n), 8.0 / 3.0 + 10.0 ** rng.uniform(-6, 2, n)),
+        (rng.uniform(-1, 1, n) * 1e-9, rng.uniform(0.1, 100.0, n)),
+        (rng.uniform(1, 2, n), rng.uniform(1, 2, n)),  # one binade: rounding-boundary stress
+    ]
+    L = _lib.load()
+    for num, den in cases:
+        num = np.ascontiguousarray(num)
+        den = np.ascontiguousarray(den)
+        bad = C.c_ulonglong(0)
+        _lib.check(L.oc_debug_lex_div(ctx.h, num.ctypes.data, den.ctypes.data, n, C.byref(bad)))
+        assert bad.value == 0
+
+
 def test_lex_sweeps_repeat_bitwise(oc, ctx):
     # the mailbox is restored after every sweep: repeated sweeps are identical
     ell = 8
