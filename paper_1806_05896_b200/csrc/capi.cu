@@ -411,7 +411,10 @@ int oc_set_tuning(const char* name, int value)
         else if (k == "cheb_block") ocb::g_cheb_block = value;
         else if (k == "fuse_norm") ocb::g_fuse_norm = value;
         else if (k == "fuse_restrict") ocb::g_fuse_restrict = value;
+        else if (k == "kkt_tiled") ocb::g_kkt_tiled = value;
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
+        // captured preconditioner graphs hold the old launch shapes: drop them
+        ocb::g_tuning_gen.fetch_add(1);
     });
 }
 
@@ -430,6 +433,7 @@ int oc_get_tuning(const char* name, int* value)
         else if (k == "cheb_block") *value = ocb::g_cheb_block;
         else if (k == "fuse_norm") *value = ocb::g_fuse_norm;
         else if (k == "fuse_restrict") *value = ocb::g_fuse_restrict;
+        else if (k == "kkt_tiled") *value = ocb::g_kkt_tiled;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);
     });
 }

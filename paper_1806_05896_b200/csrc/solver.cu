@@ -992,7 +992,8 @@ void Problem::precond_apply(int kind, const double* r, double* out)
     } else if (setup_kind_ == OC_PRECOND_PPI && !heat_) {
         throw InvalidArgument("P_D/P_T not set up");
     }
-    const long long gen = hierarchy_generation();
+    // (a tuning change alters launch shapes the captured graphs hold)
+    const long long gen = hierarchy_generation() + (g_tuning_gen.load() << 40);
     if (gen != graph_gen_) {
         drop_graphs();
         graph_gen_ = gen;
