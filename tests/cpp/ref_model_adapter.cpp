@@ -8,7 +8,8 @@
 // Cases: C1-style Poisson at level 6 (minres-pd and gmres-pt), C4-style
 // convection-diffusion (eps 0.02, SUPG) at level 6, the state-box +
 // partial-observation C3 style at level 5 with all Krylov solves converging
-// (linear_maxit 3000), and space-time heat at level 4 with 8 steps.
+// (linear_maxit 3000; faithful lexicographic smoother), and space-time heat at
+// level 4 with 8 steps.
 // Pass: u and y within 1e-10 (relative 2-norm), the objective within 1e-10,
 // the Newton count equal and every Newton solve converged.
 //
@@ -69,7 +70,7 @@ bool report(const std::string& name, const optcon::IpmResult& ref, const optcon:
 }
 
 bool steady_case(const std::string& name, optcon::ControlProblem p, int level,
-                 optcon::IpmParams params)
+                 optcon::IpmParams params, int smoother = OC_SMOOTHER_COLOR4)
 {
     const optcon::Grid g(level);
     const size_t n = static_cast<size_t>(g.num_nodes());
@@ -77,7 +78,8 @@ bool steady_case(const std::string& name, optcon::ControlProblem p, int level,
     p.f.assign(n, 0.0);
     const optcon::QpProblem qp = optcon::build_qp(p, g);
     const optcon::IpmResult ref = optcon::ipm_solve(optcon::make_steady_model(qp), params);
-    const optcon::IpmResult dev = optcon::ipm_solve(optcon_b200::make_steady_model(qp, p, g), params);
+    const optcon::IpmResult dev = optcon::ipm_solve(
+        optcon_b200::make_steady_model(qp, p, g, optcon_b200::default_context(), smoother), params);
     return report(name, ref, dev, qp.objective(ref.state.y, ref.state.z),
                   qp.objective(dev.state.y, dev.state.z));
 }
@@ -165,7 +167,12 @@ int main()
             optcon::IpmParams prm;
             prm.solver = optcon::SolverKind::gmres_ppi;
             prm.linear_maxit = 3000;
-            ok = steady_case("C3 state box + partial obs l5 gmres-ppi", p, 5, prm) && ok;
+            // the state-constrained, partially observed system pins u only to
+            // ~1e-9 at a 1e-10 Krylov residual (SURVEY §8c sensitivity table:
+            // the reference's own variants differ by 1.5e-9): the faithful
+            // lexicographic smoother reproduces the reference's preconditioner
+            ok = steady_case("C3 state box + partial obs l5 gmres-ppi (lex)", p, 5, prm,
+                             OC_SMOOTHER_LEX) && ok;
         }
         ok = heat_case("C5 heat l4 nt8 gmres-pt", 4, 8) && ok;
     } catch (const std::exception& e) {
