@@ -51,6 +51,10 @@ IPM_CASES = [
     ("c3_l6_capped", dict(pde="poisson", level=6, alpha=1e-4, beta=1e-3, u_a=-2.0, u_b=2.0,
                           y_a=-0.2, y_b=0.3, obs=(0.0, 0.5, 0.0, 1.0)),
      dict(solver="gmres-ppi", sigma=0.2, linear_maxit=15)),
+    # C3 with the reference's own cap (linear_maxit 200, ipm.hpp:27)
+    ("c3_l6_maxit200", dict(pde="poisson", level=6, alpha=1e-4, beta=1e-3, u_a=-2.0, u_b=2.0,
+                            y_a=-0.2, y_b=0.3, obs=(0.0, 0.5, 0.0, 1.0)),
+     dict(solver="gmres-ppi", sigma=0.2, linear_maxit=200)),
 ]
 
 

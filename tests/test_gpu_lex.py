@@ -141,8 +141,8 @@ def test_unknown_smoother_rejected(oc, ctx):
         oc.ipm_solve(qp, oc.IpmParams(smoother=7))
 
 
-LEX_GOLDEN = ["known_answer_l6", "c1_l6_gmres", "c1_l6_minres", "c3_l5", "c3_l6_capped", "c4_l6",
-              "c5_l5_nt16"]
+LEX_GOLDEN = ["known_answer_l6", "c1_l6_gmres", "c1_l6_minres", "c3_l5", "c3_l6_capped",
+              "c3_l6_maxit200", "c4_l6", "c5_l5_nt16"]
 
 
 @pytest.mark.parametrize("name", LEX_GOLDEN)
@@ -179,10 +179,11 @@ def test_capped_c3_needs_the_reference_smoother(oc, ctx):
     assert rel(r.u, g["u"]) > 1e-8
 
 
-def test_capped_c3_default_auto_smoother_matches_reference(oc, ctx):
+@pytest.mark.parametrize("name", ["c3_l6_capped", "c3_l6_maxit200"])
+def test_capped_c3_default_auto_smoother_matches_reference(oc, ctx, name):
     # the default smoother ("auto") redoes the first capped Newton solve with the
-    # lexicographic smoother and keeps it: the capped fixture then matches
-    g = load_golden("c3_l6_capped")
+    # lexicographic smoother and keeps it: the capped fixtures then match
+    g = load_golden(name)
     qp = qp_from_golden(oc, ctx, g)
     s = g["meta"]["solve"]
     r = oc.ipm_solve(qp, oc.IpmParams(sigma=s["sigma"], solver=s["solver"],
