@@ -5,18 +5,45 @@
 #include "solver.hpp"
 
 #include <cstring>
+#include <mutex>
 #include <string>
 
+// Lifetime: every problem and hierarchy holds its context's stream and pools
+// (ocb::Ctx&), so a context is deleted only after its last child: oc_destroy
+// on a context with live children marks it closing, and the last child's
+// destroy deletes it (a façade context dying before its QpProblem).
 struct oc_ctx {
     ocb::Ctx ctx;
+    int children = 0;     // live problems and hierarchies (guarded by g_life)
+    bool closing = false; // oc_destroy called while children were live
     explicit oc_ctx(int dev) : ctx(dev) {}
 };
 
+namespace {
+std::mutex g_life;
+void ctx_adopt(oc_ctx* c)
+{
+    std::lock_guard<std::mutex> lk(g_life);
+    ++c->children;
+}
+void ctx_release(oc_ctx* c)
+{
+    bool del = false;
+    {
+        std::lock_guard<std::mutex> lk(g_life);
+        del = --c->children == 0 && c->closing;
+    }
+    if (del) delete c;
+}
+} // namespace
+
 struct oc_problem {
     std::unique_ptr<ocb::Problem> p;
+    oc_ctx* owner = nullptr;
 };
 
 struct oc_mg {
+    oc_ctx* owner = nullptr;
     ocb::Ctx* ctx = nullptr;
     int level = 0;
     ocb::DVec fine;
@@ -70,7 +97,18 @@ int oc_create(oc_ctx** out, int device)
     });
 }
 
-void oc_destroy(oc_ctx* c) { delete c; }
+void oc_destroy(oc_ctx* c)
+{
+    if (!c) return;
+    {
+        std::lock_guard<std::mutex> lk(g_life);
+        if (c->children > 0) {
+            c->closing = true; // the last problem / hierarchy deletes it
+            return;
+        }
+    }
+    delete c;
+}
 
 int oc_synchronize(oc_ctx* c)
 {
@@ -88,11 +126,19 @@ int oc_problem_create(oc_ctx* c, const oc_problem_desc* d, oc_problem** out)
         require(out, "oc_problem_create");
         auto p = std::make_unique<oc_problem>();
         p->p = std::make_unique<ocb::Problem>(c->ctx, *d);
+        p->owner = c;
+        ctx_adopt(c);
         *out = p.release();
     });
 }
 
-void oc_problem_destroy(oc_problem* p) { delete p; }
+void oc_problem_destroy(oc_problem* p)
+{
+    if (!p) return;
+    oc_ctx* owner = p->owner;
+    delete p;
+    if (owner) ctx_release(owner);
+}
 
 int oc_problem_info_get(oc_problem* p, oc_problem_info* info)
 {
@@ -296,6 +342,8 @@ int oc_mg_create(oc_ctx* c, int level, const double* coef9, int rediscretize, do
         m->t0.resize((size_t)n);
         m->t1.resize((size_t)n);
         c->ctx.sync();
+        m->owner = c;
+        ctx_adopt(c);
         *out = m.release();
     });
 }
@@ -352,8 +400,11 @@ int oc_mg_smooth(oc_mg* m, const double* b, double* x, int forward)
 
 void oc_mg_destroy(oc_mg* m)
 {
-    if (m && m->ctx) cudaStreamSynchronize(m->ctx->stream);
+    if (!m) return;
+    if (m->ctx) cudaStreamSynchronize(m->ctx->stream);
+    oc_ctx* owner = m->owner;
     delete m;
+    if (owner) ctx_release(owner);
 }
 
 int oc_cheb_apply(oc_ctx* c, int level, double scale, const double* extra, int steps,

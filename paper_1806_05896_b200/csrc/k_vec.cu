@@ -531,10 +531,15 @@ bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, co
 {
     constexpr size_t smem = ((size_t)(kMgsBlocks / 148) * kMgsSmemM * 256 + kMgsBlocks) * sizeof(double);
     // one CTA per SM on a 148-SM B200, all co-resident; otherwise the caller
-    // runs the launch-per-step sequence (same bits)
-    static const bool ok = [] {
-        int dev = 0, sms = 0, per_sm = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    // runs the launch-per-step sequence (same bits). Checked (and the shared
+    // memory attribute set) once per device: 0 unknown, 1 usable, 2 not.
+    static std::atomic<int> state[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    int st = state[dev].load();
+    if (st == 0) {
+        st = [dev] {
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms != 148 || kMgsBlocks % sms || (kMgsBlocks / sms) % (kMgsPersistThreads / 256)) return false;
         if (cudaFuncSetAttribute(k_mgs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -543,8 +548,10 @@ bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, co
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_persistent, kMgsPersistThreads, smem);
         cudaGetLastError();
         return per_sm >= 1;
-    }();
-    if (!ok || n > (long long)kMgsPersistM * kMgsBlocks * 256) return false;
+        }() ? 1 : 2;
+        state[dev].store(st);
+    }
+    if (st != 1 || n > (long long)kMgsPersistM * kMgsBlocks * 256) return false;
     note_launch();
     double* H = G.H;
     int ld = G.ld;
@@ -553,8 +560,12 @@ bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, co
                     (void*)&pa, (void*)&pb, (void*)&pfinal, (void*)&bar, (void*)&n};
     const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_mgs_persistent, dim3(148),
                                                       dim3(kMgsPersistThreads), args, smem, s);
-    if (e != cudaSuccess)
-        throw std::runtime_error(std::string("k_mgs_persistent: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+        // e.g. the SMs are shared with another context's kernels and the 148
+        // CTAs cannot all be resident: fall back to the launch-per-step path
+        cudaGetLastError();
+        return false;
+    }
     return true;
 }
 
