@@ -219,6 +219,8 @@ int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
  * coefficient copy), "cheb_block" (1: 5 Chebyshev steps per launch),
  * "fuse_norm" (1: a V-cycle's last sweep launch runs the divergence check),
  * "kkt_tiled" (1: the steady KKT apply from shared-memory halo tiles),
+ * "lex_bottom_top" (lexicographic mode: top level of the single-CTA bottom
+ * solver, 3..6, default 4; higher levels sweep as multi-CTA wavefronts),
  * "fuse_restrict" (1: a level's last pre-smoothing launch restricts its
  * residual), "mgs_persistent" (GMRES columns with j+1 >= value run their
  * modified Gram-Schmidt in one cooperative launch; default 8, 0 never).

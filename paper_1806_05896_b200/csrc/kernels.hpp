@@ -23,6 +23,7 @@ struct MgLevelDev {
 
 constexpr int kBottomMaxLevels = 7;   // levels 2..8 at most (cluster kernel with a level-8 top)
 constexpr int kBottomTopLevel = 6;    // grid levels <= this run inside one CTA
+extern std::atomic<int> g_lex_bottom_top; // lexicographic mode: top level of the single-CTA bottom (4)
 
 struct BottomArgs {
     int nlev;                          // number of levels handled (top .. level 2)

@@ -175,7 +175,10 @@ void Hierarchy::allocate(int level, int batch, int smoother)
     // (the cluster kernel smooths with 4 colours; the lexicographic mode keeps
     // levels <= 6 in the single-CTA kernel and sweeps the others as wavefronts)
     cluster_ = !lex_ && g_cluster_bottom && level >= 6 && cluster_bottom_supported();
-    const int top = cluster_ ? kClusterTopLevel : kBottomTopLevel;
+    // (lexicographic mode: levels 6 and 5 as wavefront bands of k_gs_lex,
+    // faster than the single CTA's two warps streaming their coefficients;
+    // C3 P_Pi apply 101 -> 92 ms)
+    const int top = cluster_ ? kClusterTopLevel : (lex_ ? g_lex_bottom_top.load() : kBottomTopLevel);
     kb_ = 0;
     while (level - kb_ > top) ++kb_;
     coef_.clear();

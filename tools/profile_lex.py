@@ -13,6 +13,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1806_05896_b200 import configs, optcon as oc  # noqa: E402
 
 KIND = {"gmres-pt": "pt", "minres-pd": "pd", "gmres-ppi": "ppi"}
+args = sys.argv[1:]
+while args[:1] == ["--tune"]:  # --tune name=value (oc_set_tuning knob)
+    from paper_1806_05896_b200 import _lib
+
+    key, v = args[1].split("=")
+    _lib.check(_lib.load().oc_set_tuning(key.encode(), int(v)))
+    args = args[2:]
+sys.argv = sys.argv[:1] + args
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 smoother = sys.argv[2] if len(sys.argv) > 2 else "lex"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
