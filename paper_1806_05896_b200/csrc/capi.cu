@@ -463,6 +463,7 @@ int oc_set_tuning(const char* name, int value)
         else if (k == "fuse_norm") ocb::g_fuse_norm = value;
         else if (k == "fuse_restrict") ocb::g_fuse_restrict = value;
         else if (k == "kkt_tiled") ocb::g_kkt_tiled = value;
+        else if (k == "heat_fork") ocb::g_heat_fork = value;
         else if (k == "lex_bottom_top") ocb::g_lex_bottom_top = value < 3 ? 3 : (value > 6 ? 6 : value);
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
         // captured preconditioner graphs hold the old launch shapes: drop them
@@ -486,6 +487,7 @@ int oc_get_tuning(const char* name, int* value)
         else if (k == "fuse_norm") *value = ocb::g_fuse_norm;
         else if (k == "fuse_restrict") *value = ocb::g_fuse_restrict;
         else if (k == "kkt_tiled") *value = ocb::g_kkt_tiled;
+        else if (k == "heat_fork") *value = ocb::g_heat_fork;
         else if (k == "lex_bottom_top") *value = ocb::g_lex_bottom_top;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);
     });

@@ -166,6 +166,7 @@ void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const d
                       int steps, const ChebWork& w, double* out);
 extern std::atomic<int> g_cheb_block; // 1: up to 5 Chebyshev steps per launch (temporal blocking)
 extern std::atomic<int> g_kkt_tiled;  // 1: steady KKT apply from shared-memory halo tiles
+extern std::atomic<int> g_heat_fork;  // 1: heat P_D's time-block substitution on the high-priority side stream
 extern std::atomic<long long> g_tuning_gen; // bumped by every oc_set_tuning (invalidates graphs)
 extern std::atomic<int> g_fuse_norm;  // 1: a V-cycle's last sweep launch runs the divergence check
 extern std::atomic<int> g_fuse_restrict; // 1: a level's last pre-smoothing launch restricts the residual

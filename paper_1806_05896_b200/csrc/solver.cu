@@ -114,6 +114,11 @@ Ctx::Ctx(int dev) : device(dev)
     if (dev < 0 || dev >= count) throw CudaFailure("oc_create: no such CUDA device");
     cuda_check(cudaSetDevice(dev), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    int lo = 0, hi = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+    cuda_check(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaEventCreate(&ev0), "cudaEventCreate");
     cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
     for (auto& e : user_ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
@@ -133,6 +138,12 @@ Ctx::~Ctx()
     for (auto& e : user_ev)
         if (e) cudaEventDestroy(e);
     for (auto& g : spare_graphs) cudaGraphExecDestroy(g.exec);
+    if (side) {
+        cudaStreamSynchronize(side);
+        cudaStreamDestroy(side);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -1074,6 +1085,29 @@ void Problem::precond_apply_direct(int kind, const double* r, double* out)
     if (setup_kind_ == OC_PRECOND_PPI && !heat_) throw InvalidArgument("P_D/P_T not set up");
     // BlockDiagPrecond (precond.cpp:202-212) / BlockTriPrecond (:214-230)
     ChebWork w{cg_.get(), c0_.get(), c1_.get(), c2_.get()};
+    if (heat_ && kind == OC_PRECOND_PD && g_heat_fork.load()) {
+        // P_D's three blocks are independent: the time-block substitution (256
+        // dependent cluster launches) runs on the high-priority side stream
+        // while Chebyshev and the 2x2 blocks run here; with several solves in
+        // flight the priority lets the cluster launches claim their SMs ahead
+        // of other solves' wide kernels
+        cuda_check(cudaEventRecord(ctx.ev_fork, ctx.stream), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(ctx.side, ctx.ev_fork, 0), "cudaStreamWaitEvent");
+        std::swap(ctx.stream, ctx.side);
+        try {
+            schur_apply(rp, op);
+        } catch (...) {
+            std::swap(ctx.stream, ctx.side);
+            throw;
+        }
+        std::swap(ctx.stream, ctx.side);
+        launch_chebyshev(ctx.stream, P, ry, ty, cheb_steps_, w, oy);
+        launch_control_2x2(ctx.stream, P, tw_.get(), tv_.get(), rw, rv, ow, ov, fl);
+        cuda_check(cudaEventRecord(ctx.ev_join, ctx.side), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(ctx.stream, ctx.ev_join, 0), "cudaStreamWaitEvent");
+        launch_check("block preconditioner apply");
+        return;
+    }
     launch_chebyshev(ctx.stream, P, ry, ty, cheb_steps_, w, oy);
     launch_control_2x2(ctx.stream, P, tw_.get(), tv_.get(), rw, rv, ow, ov, fl);
     if (kind == OC_PRECOND_PT) {

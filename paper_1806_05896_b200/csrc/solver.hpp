@@ -99,6 +99,11 @@ struct Profiler {
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // high-priority side stream: the heat time-block substitution of a P_D
+    // apply runs on it, forked from / joined to `stream` by two events, while
+    // the Chebyshev and 2x2 blocks run on `stream`
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t user_ev[8] = {};
     double* hscal = nullptr; // pinned host mirror (64 doubles)

@@ -1,7 +1,7 @@
 """Throughput of R independent C5 solves in flight on one GPU (one context,
 stream and host thread each; y_d seeds 42..42+R-1), R from the command line.
 
-    python tools/c5_concurrency.py 1 2 4 8
+    python tools/c5_concurrency.py [--tune name=value] 1 2 4 8
 """
 import os
 import sys
@@ -12,8 +12,15 @@ import torch  # noqa: E402
 
 from paper_1806_05896_b200 import configs, optcon as oc, replicas  # noqa: E402
 
+args = sys.argv[1:]
+while args[:1] == ["--tune"]:  # --tune name=value (oc_set_tuning knob)
+    from paper_1806_05896_b200 import _lib
+
+    key, v = args[1].split("=")
+    _lib.check(_lib.load().oc_set_tuning(key.encode(), int(v)))
+    args = args[2:]
 c = configs.C5
-for R in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]:
+for R in [int(a) for a in args] or [1, 2, 4, 8]:
     ctxs = [oc.Context(0) for _ in range(R)]
     qps = []
     for i in range(R):
