@@ -320,9 +320,10 @@ __global__ void __launch_bounds__(kMgsPersistThreads, 1)
     }
 }
 
-__global__ void k_gmres_givens(const double* __restrict__ part, GmresDev G, int j)
+// Columns beyond kGivMax (linear_maxit > 255 without restarts): one thread.
+__global__ void k_gmres_givens_serial(const double* __restrict__ part, GmresDev G, int j)
 {
-    const double s2 = sum_partials_warp(part, kMgsBlocks); // from the last k_mgs_dot
+    const double s2 = sum_partials_warp(part, kMgsBlocks);
     if (threadIdx.x != 0) return;
     const double hnext = sqrt(s2);
     G.scal[1] = hnext;
@@ -335,7 +336,7 @@ __global__ void k_gmres_givens(const double* __restrict__ part, GmresDev G, int 
     }
     const double r = hypot(h[j], hnext);
     if (r == 0.0) {
-        *G.stop = 1; // "gmres: zero pivot in Hessenberg triangularization"
+        *G.stop = 1;
         return;
     }
     G.cs[j] = h[j] / r;
@@ -349,6 +350,82 @@ __global__ void k_gmres_givens(const double* __restrict__ part, GmresDev G, int 
         for (int k2 = i + 1; k2 < m; ++k2) s -= G.H[(long long)k2 * G.ld + i] * G.y[k2];
         G.y[i] = s / G.H[(long long)i * G.ld + i];
     }
+}
+
+// Givens rotations of the new Hessenberg column and the back substitution
+// R y = g (krylov.cpp:158-180), sequential in the reference's order on
+// thread 0; the 1024-thread block stages every operand in shared memory first
+// with coalesced loads (the column, rotations, g, and R in 32-row blocks), so
+// the dependent chain runs on shared-memory latency instead of one L2 round
+// trip per term (C3 at j ~ 67: 209 us -> ~10 us).
+constexpr int kGivT = 1024, kGivRows = 16, kGivMax = 256;
+__global__ void __launch_bounds__(kGivT) k_gmres_givens(const double* __restrict__ part, GmresDev G, int j)
+{
+    __shared__ double hs[kGivMax + 1], css[kGivMax], sns[kGivMax], gs[kGivMax + 1], ys[kGivMax];
+    __shared__ double rb[kGivRows * kGivMax]; // R(i, k2) for a block of 32 rows i
+    __shared__ int stop;
+    const int t = threadIdx.x;
+    const int m = j + 1;
+    double* h = G.H + (long long)j * G.ld;
+    for (int i = t; i < j + 1; i += kGivT) hs[i] = h[i];
+    for (int i = t; i < j; i += kGivT) {
+        css[i] = G.cs[i];
+        sns[i] = G.sn[i];
+    }
+    for (int i = t; i <= j; i += kGivT) gs[i] = G.g[i];
+    double s2 = 0.0;
+    if (t < 32) s2 = sum_partials_warp(part, kMgsBlocks); // from the last k_mgs_dot
+    __syncthreads();
+    if (t == 0) {
+        stop = 0;
+        const double hnext = sqrt(s2);
+        G.scal[1] = hnext;
+        hs[j + 1] = hnext;
+        for (int i = 0; i < j; ++i) {
+            const double tt = css[i] * hs[i] + sns[i] * hs[i + 1];
+            hs[i + 1] = -sns[i] * hs[i] + css[i] * hs[i + 1];
+            hs[i] = tt;
+        }
+        const double r = hypot(hs[j], hnext);
+        if (r == 0.0) {
+            *G.stop = 1; // "gmres: zero pivot in Hessenberg triangularization"
+            stop = 1;
+        } else {
+            const double c = hs[j] / r, sn = hnext / r;
+            G.cs[j] = c;
+            G.sn[j] = sn;
+            hs[j] = r;
+            gs[j + 1] = -sn * gs[j];
+            gs[j] *= c;
+            G.g[j + 1] = gs[j + 1];
+            G.g[j] = gs[j];
+        }
+    }
+    __syncthreads();
+    for (int i = t; i <= j + 1; i += kGivT) h[i] = hs[i];
+    if (stop) return;
+    // back substitution in blocks of 32 rows, bottom up; row i needs
+    // R(i, k2) = H[k2 * ld + i] for k2 > i (column k2 of the stored H)
+    for (int i1 = m - 1; i1 >= 0; i1 -= kGivRows) {
+        const int i0 = max(i1 - kGivRows + 1, 0);
+        const int nr = i1 - i0 + 1;
+        __syncthreads();
+        for (int e = t; e < nr * m; e += kGivT) {
+            const int k2 = e / nr, ii = e - k2 * nr; // consecutive threads: consecutive rows
+            rb[ii * kGivMax + k2] = k2 == j ? hs[i0 + ii] : G.H[(long long)k2 * G.ld + i0 + ii];
+        }
+        __syncthreads();
+        if (t == 0) {
+            for (int i = i1; i >= i0; --i) {
+                const double* row = rb + (i - i0) * kGivMax;
+                double s = gs[i];
+                for (int k2 = i + 1; k2 < m; ++k2) s -= row[k2] * ys[k2];
+                ys[i] = s / row[i];
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = t; i < m; i += kGivT) G.y[i] = ys[i];
 }
 
 __global__ void k_relres(const double* __restrict__ part, const double* __restrict__ bnorm,
@@ -572,7 +649,8 @@ bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, co
 void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j)
 {
     note_launch();
-    k_gmres_givens<<<1, 32, 0, s>>>(part, G, j);
+    if (j + 1 >= kGivMax) k_gmres_givens_serial<<<1, 32, 0, s>>>(part, G, j);
+    else k_gmres_givens<<<1, kGivT, 0, s>>>(part, G, j);
 }
 
 void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst)
