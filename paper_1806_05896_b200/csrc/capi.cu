@@ -464,6 +464,7 @@ int oc_set_tuning(const char* name, int value)
         else if (k == "fuse_restrict") ocb::g_fuse_restrict = value;
         else if (k == "kkt_tiled") ocb::g_kkt_tiled = value;
         else if (k == "heat_fork") ocb::g_heat_fork = value;
+        else if (k == "lex_start") ocb::g_lex_start = value < 17 ? 17 : value;
         else if (k == "lex_bottom_top") ocb::g_lex_bottom_top = value < 3 ? 3 : (value > 6 ? 6 : value);
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
         // captured preconditioner graphs hold the old launch shapes: drop them
@@ -488,6 +489,7 @@ int oc_get_tuning(const char* name, int* value)
         else if (k == "fuse_restrict") *value = ocb::g_fuse_restrict;
         else if (k == "kkt_tiled") *value = ocb::g_kkt_tiled;
         else if (k == "heat_fork") *value = ocb::g_heat_fork;
+        else if (k == "lex_start") *value = ocb::g_lex_start;
         else if (k == "lex_bottom_top") *value = ocb::g_lex_bottom_top;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);
     });

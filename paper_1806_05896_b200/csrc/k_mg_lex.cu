@@ -101,6 +101,7 @@ struct LexArgs {
     double* x;
     double* mbox;
     int* flags;
+    int start_col; // column of the band above that starts a band (hand-over lag)
 };
 
 template <bool VAR, bool FWD>
@@ -230,9 +231,10 @@ __global__ void __launch_bounds__(LexSlot<VAR>::kThreads, 1) k_gs_lex(LexArgs a)
         load(2, B0{});
         load(3, B1{});
         if (consumer && sw == 0) {
-            // start once the band above has produced column 32 (its lag keeps
-            // every later mailbox chunk ahead of this band's need)
-            const int xs = min(2 * kLW, nx - 1);
+            // start once the band above has produced column g_lex_start (the
+            // lag this sets keeps the next mailbox chunk, fetched at the end
+            // of each period, about ready when it is fetched)
+            const int xs = min(a.start_col, nx - 1);
             while (lex_is_sentinel(ld_relaxed(mb_in + xs))) {
                 if (++stall > kLexSpinLimit) {
                     if (j == 0) atomicOr(a.flags, kErrLexStall);
@@ -385,6 +387,7 @@ void go(cudaStream_t s, const LexArgs& a)
 } // namespace
 
 std::atomic<int> g_lex_bottom_top{4};
+std::atomic<int> g_lex_start{32};
 
 void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                    const double* dfull, double* x, bool forward, double* mbox, int* flags)
@@ -399,6 +402,7 @@ void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* 
     a.x = x;
     a.mbox = mbox;
     a.flags = flags;
+    a.start_col = g_lex_start.load();
     note_launch();
     if (A.coef) {
         if (forward) go<true, true>(s, a);

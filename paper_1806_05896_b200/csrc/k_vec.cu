@@ -429,10 +429,16 @@ __global__ void __launch_bounds__(kGivT) k_gmres_givens(const double* __restrict
 }
 
 __global__ void k_relres(const double* __restrict__ part, const double* __restrict__ bnorm,
-                         double* dst)
+                         double* dst, const int* flags, const int* stop, double* status)
 {
     const double s = sum_partials_warp(part, kRedBlocks);
-    if (threadIdx.x == 0) dst[0] = sqrt(s) / bnorm[0];
+    if (threadIdx.x == 0) {
+        dst[0] = sqrt(s) / bnorm[0];
+        if (status) { // the iteration's error flags and stop code next to the scalars:
+            status[0] = (double)(flags ? flags[0] : 0); // one readback per Krylov iteration
+            status[1] = (double)(stop ? stop[0] : 0);
+        }
+    }
 }
 
 // MINRES scalar slots
@@ -653,10 +659,11 @@ void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, 
     else k_gmres_givens<<<1, kGivT, 0, s>>>(part, G, j);
 }
 
-void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst)
+void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst,
+                   const int* flags, const int* stop, double* status)
 {
     note_launch();
-    k_relres<<<1, 32, 0, s>>>(part, bnorm, dst);
+    k_relres<<<1, 32, 0, s>>>(part, bnorm, dst, flags, stop, status);
 }
 
 void launch_minres_setup(cudaStream_t s, const double* part, double* sc)

@@ -24,6 +24,7 @@ struct MgLevelDev {
 constexpr int kBottomMaxLevels = 7;   // levels 2..8 at most (cluster kernel with a level-8 top)
 constexpr int kBottomTopLevel = 6;    // grid levels <= this run inside one CTA
 extern std::atomic<int> g_lex_bottom_top; // lexicographic mode: top level of the single-CTA bottom (4)
+extern std::atomic<int> g_lex_start;      // lexicographic sweep: band start column of the band above
 
 struct BottomArgs {
     int nlev;                          // number of levels handled (top .. level 2)
@@ -253,7 +254,9 @@ bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, co
 // hnext from partials -> H(j+1, j), Givens update and back substitution for y (one thread)
 void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j);
 // scal[2] = sqrt(sum part) / bnorm
-void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst);
+// (status != nullptr: also status[0] = flags[0], status[1] = stop[0], as doubles)
+void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst,
+                   const int* flags = nullptr, const int* stop = nullptr, double* status = nullptr);
 
 // ----------------------------------------------------------------- MINRES
 // scalar state (krylov.cpp:37-131): see k_vec.cu for the slot layout

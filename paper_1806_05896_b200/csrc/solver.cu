@@ -1227,15 +1227,14 @@ oc_solve_report Problem::gmres(const oc_ipm_params& p, int kind, const double* b
                            xbase ? kx2_.get() : nullptr);
             launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(), x,
                        nullptr, b, part);
-            launch_relres(ctx.stream, part, scal + 0, scal + 2);
+            // one packed readback per iteration: scalars, error flags, stop code
+            launch_relres(ctx.stream, part, scal + 0, scal + 2, flags_.get(), stop_.get(), scal + 8);
             launch_check("gmres iteration");
-            cuda_check(cudaMemcpyAsync(ctx.hscal, scal, 4 * sizeof(double), cudaMemcpyDeviceToHost,
+            cuda_check(cudaMemcpyAsync(ctx.hscal, scal, 10 * sizeof(double), cudaMemcpyDeviceToHost,
                                        ctx.stream), "readback");
-            cuda_check(cudaMemcpyAsync(ctx.hflags, flags_.get(), sizeof(int),
-                                       cudaMemcpyDeviceToHost, ctx.stream), "readback");
-            cuda_check(cudaMemcpyAsync(ctx.hflags + 1, stop_.get(), sizeof(int),
-                                       cudaMemcpyDeviceToHost, ctx.stream), "readback");
             ctx.sync();
+            ctx.hflags[0] = (int)ctx.hscal[8];
+            ctx.hflags[1] = (int)ctx.hscal[9];
             check_flags(false);
             const double hnext = ctx.hscal[1];
             const double relres = ctx.hscal[2];
@@ -1337,15 +1336,15 @@ oc_solve_report Problem::minres(const oc_ipm_params& p, int kind, const double* 
         launch_minres_update(ctx.stream, z, wprev, w, wnext, x, sc, stop, n);
         launch_minres_rotate(ctx.stream, sc, stop);
         launch_kkt(ctx.stream, P, tyk, tw_.get(), tv_.get(), x, nullptr, b, part);
-        launch_relres(ctx.stream, part, scal_.get() + 0, scal_.get() + 2);
+        // one packed readback per iteration: scalars, error flags, stop code
+        launch_relres(ctx.stream, part, scal_.get() + 0, scal_.get() + 2, flags_.get(), stop,
+                      scal_.get() + 8);
         launch_check("minres iteration");
-        cuda_check(cudaMemcpyAsync(ctx.hscal, scal_.get(), 48 * sizeof(double),
+        cuda_check(cudaMemcpyAsync(ctx.hscal, scal_.get(), 17 * sizeof(double), // + gamma (sc[0])
                                    cudaMemcpyDeviceToHost, ctx.stream), "readback");
-        cuda_check(cudaMemcpyAsync(ctx.hflags, flags_.get(), sizeof(int), cudaMemcpyDeviceToHost,
-                                   ctx.stream), "readback");
-        cuda_check(cudaMemcpyAsync(ctx.hflags + 1, stop, sizeof(int), cudaMemcpyDeviceToHost,
-                                   ctx.stream), "readback");
         ctx.sync();
+        ctx.hflags[0] = (int)ctx.hscal[8];
+        ctx.hflags[1] = (int)ctx.hscal[9];
         check_flags(false);
         const double relres = ctx.hscal[2];
         const int st = ctx.hflags[1];

@@ -4,8 +4,9 @@ reference runs on the host cores (one process per case, in parallel).
 
     python tools/parity_full.py [--out gpurun_out/parity_full.json] [cases...]
 
-Cases: C1, C2 (9 cells), C4, C5, C3@8 (C3 at level 8: the reference needs
-~1-2 h at 1025^2). Bar (north_star): u, y, J to rel 1e-8, NLI +-1, zero-count
+Cases: C1, C2 (9 cells), C4, C5 (gmres-pt, reference-native), C5m (C5 with
+block-diagonal MINRES against the reference-class composition), C3@8 (C3 at
+level 8: the reference needs ~1.4 h at 1025^2). Bar (north_star): u, y, J to rel 1e-8, NLI +-1, zero-count
 and active sets exact.
 """
 import argparse
@@ -28,6 +29,8 @@ def case_list(names):
     for nm in names:
         if nm == "C2":
             out += [(f"C2[{i}]", c) for i, c in enumerate(configs.C2_CELLS)]
+        elif nm == "C5m":  # C5 with the solver BASELINE names (block-diagonal MINRES)
+            out.append((nm, configs.C5.with_level(8, solver="minres-pd")))
         elif "@" in nm:
             base, lvl = nm.split("@")
             out.append((nm, configs.ALL[base].with_level(int(lvl))))
@@ -56,7 +59,9 @@ def run_ref(args):
         kw["obs"] = c.obs
     t0 = time.perf_counter()
     P = ref.RefProblem(c.pde, c.level, **kw)
-    r = P.solve(c.solver, sigma=c.sigma)
+    # heat MINRES-P_D: the reference-class composition
+    solver = "heat-minres-pd" if c.pde == "heat" and c.solver == "minres-pd" else c.solver
+    r = P.solve(solver, sigma=c.sigma)
     return name, dict(u=r.u, y=r.y, z=r.z, nli=r.nli, av_li=r.av_li, objective=r.objective,
                       converged=r.converged, seconds=time.perf_counter() - t0,
                       lin=[d["lin_iters"] for d in r.records[1:]],
@@ -114,7 +119,7 @@ def main():
     ap.add_argument("cases", nargs="*", default=["C1", "C2", "C4", "C5", "C3@8"])
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "parity_full.json"))
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 4)
-    ap.add_argument("--smoother", default="color4", help="color4 | lex (faithful mode)")
+    ap.add_argument("--smoother", default="auto", help="auto (default) | color4 | lex (faithful mode)")
     a = ap.parse_args()
     cases = case_list(a.cases)
     gpu = run_gpu(cases, a.smoother)
