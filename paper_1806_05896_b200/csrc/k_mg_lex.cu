@@ -387,7 +387,7 @@ void go(cudaStream_t s, const LexArgs& a)
 } // namespace
 
 std::atomic<int> g_lex_bottom_top{4};
-std::atomic<int> g_lex_start{32};
+std::atomic<int> g_lex_start{17};
 
 void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* inv,
                    const double* dfull, double* x, bool forward, double* mbox, int* flags)
