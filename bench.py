@@ -345,6 +345,23 @@ def measured_traffic(kernel):
     return best
 
 
+def reference_solve_time(case):
+    """The reference's full IPM solve time for a BASELINE case, measured on a
+    host of this pool by tools/parity_full.py (profiles/*/parity_full_r*.json),
+    with its Newton and average Krylov counts; None when not recorded."""
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "parity_full_r*.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        if case in d and "ref_s" in d[case]:
+            r = d[case]
+            best = {"seconds": r["ref_s"], "nli": r["nli"][1], "av_li": r["av_li"][1],
+                    "source": os.path.relpath(f, ROOT)}
+    return best
+
+
 # ------------------------------------------------------------------ ours
 def _setup_torch(args):
     import torch
@@ -556,6 +573,7 @@ def run_ours_c5(args, torch, dist, rank, world, local):
                          "krylov_iters_per_s": single.total_lin / (single.solve_ms / 1e3),
                          "nli": single.stats.nli, "av_li": round(single.stats.av_li, 3),
                          "note": "seed 42 alone on the GPU (untimed pass)"},
+        "time_to_solution_vs_reference": _tts(single, "C5m" if args.solver == "minres-pd" else "C5"),
         "nli": [r.stats.nli for r in results[-1]], "av_li": [round(r.stats.av_li, 3) for r in results[-1]],
         "lin_iters_seed42": [i.lin_iters for i in last.stats.iterations[1:]],
         "objective_seed42": last.objective,
@@ -564,6 +582,20 @@ def run_ours_c5(args, torch, dist, rank, world, local):
                               "how": "oc_time_applies on replica 0 alone after its last solve "
                                      "(final Theta), CUDA events; SURVEY 8d byte model"},
     }
+
+
+def _tts(single, case):
+    """One solve's IPM time to tolerance against the reference's full solve of
+    the same case (one host thread, recorded by tools/parity_full.py): the
+    speed-up that counts each side's own Krylov iterations."""
+    ref = reference_solve_time(case)
+    if not ref:
+        return None
+    return {"device_s": single.solve_ms / 1e3, "reference_s": ref["seconds"],
+            "ratio": ref["seconds"] / (single.solve_ms / 1e3),
+            "device_nli_av_li": [single.stats.nli, round(single.stats.av_li, 3)],
+            "reference_nli_av_li": [ref["nli"], ref["av_li"]], "reference_source": ref["source"],
+            "note": "reference: one host thread of this pool, recorded (not re-run by the bench)"}
 
 
 def run_ours_c2(args, torch, dist, rank, world, local):

@@ -9,6 +9,8 @@
 //   minres / gmres                 krylov.cpp:37-212
 #include "solver.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -23,6 +25,16 @@
 #include <cstring>
 
 namespace ocb {
+
+// NVTX ranges around the solver phases (ipm_solve, each Newton step's
+// preconditioner setup and Krylov solve): visible in Nsight timelines,
+// a no-op without an attached tool
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 void cuda_check(cudaError_t e, const char* what)
 {
@@ -805,6 +817,7 @@ void Problem::kkt(const double* x, double* out)
 
 void Problem::setup_precond(int kind, const oc_ipm_params& p)
 {
+    Nvtx nv("precond_setup");
     if (p.cheb_steps < 1) throw InvalidArgument("chebyshev: steps must be >= 1");
     mg_.cycles = p.mg_cycles;
     mg_.pre = p.mg_pre;
@@ -1151,6 +1164,7 @@ void Problem::ensure_krylov(size_t count)
 
 oc_solve_report Problem::gmres(const oc_ipm_params& p, int kind, const double* b, double* x)
 {
+    Nvtx nv("gmres");
     // krylov.cpp:133-212 (full GMRES; optional restart every p.gmres_restart)
     oc_solve_report rep{};
     const long long n = 4 * ny_;
@@ -1274,6 +1288,7 @@ oc_solve_report Problem::gmres(const oc_ipm_params& p, int kind, const double* b
 
 oc_solve_report Problem::minres(const oc_ipm_params& p, int kind, const double* b, double* x)
 {
+    Nvtx nv("minres");
     // krylov.cpp:37-131
     oc_solve_report rep{};
     const long long n = 4 * ny_;
@@ -1409,6 +1424,7 @@ oc_solve_report Problem::newton_solve(const oc_ipm_params& p, const double* rhs,
 
 void Problem::ipm_solve(const oc_ipm_params& p, oc_ipm_result* r)
 {
+    Nvtx nv("ipm_solve");
     // ipm_solve (ipm.cpp:270-341)
     if (!(p.alpha0 > 0.0 && p.alpha0 < 1.0))
         throw InvalidArgument("ipm_solve: alpha0 must lie in (0,1)");
