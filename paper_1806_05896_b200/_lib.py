@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liboptcon_b200.so")
+# OPTCON_B200_LIB: another build of the same library (A/B runs of tools/ab_lib.py)
+LIB_PATH = os.environ.get("OPTCON_B200_LIB") or os.path.join(_HERE, "_lib", "liboptcon_b200.so")
 
 OC_OK, OC_INVALID_ARGUMENT, OC_RUNTIME_ERROR, OC_CUDA_ERROR = 0, 1, 2, 3
 

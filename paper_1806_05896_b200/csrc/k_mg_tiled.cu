@@ -78,13 +78,27 @@ struct SweepShape {
     static constexpr int H = 4 * NS + (MODE ? 2 : 0);
     static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
     static constexpr int R = RX * RY;
+    // Shared-memory layout: colour-planar. Plane c = (lx & 1) + 2 (ly & 1) holds
+    // the region nodes of one colour, row-major over the colour sub-lattice
+    // (CXN x CYN), so a colour pass reads every operand at unit stride (the
+    // natural layout reads every other word: two-way bank conflicts on each
+    // 64-bit access). The plane stride is padded to 8 mod 16 words so the
+    // staging copies (lanes alternate between two planes) stay conflict-free.
+    static constexpr int CXN = RX / 2, CYN = RY / 2, KC = CXN * CYN;
+    static constexpr int PS = KC + (24 - KC % 16) % 16;
+    static constexpr int RP = 4 * PS; // words per staged field
     // variable coefficients are staged in shared memory whenever the 11 planes
     // fit (coalesced row copies, read once per launch for all fused sweeps);
     // otherwise read through L1 (colour-strided, L2-bandwidth bound)
-    static constexpr bool CS = VAR && (size_t)11 * R * sizeof(double) <= 100 * 1024; // >= 2 CTAs/SM
+    static constexpr bool CS = VAR && (size_t)11 * RP * sizeof(double) <= 100 * 1024; // >= 2 CTAs/SM
     static constexpr int PLANES = CS ? 11 : 3; // x, b, inv (+ 8 off-diagonals)
     static constexpr int RSX = TX + 1, RSN = (TX + 1) * (TY + 1); // MODE 2: fine residual rows
-    static constexpr size_t smem = ((size_t)PLANES * R + (MODE == 2 ? RSN : 0)) * sizeof(double);
+    static constexpr size_t smem = ((size_t)PLANES * RP + (MODE == 2 ? RSN : 0)) * sizeof(double);
+    // planar index of region node (lx, ly)
+    __host__ __device__ static constexpr int pidx(int lx, int ly)
+    {
+        return ((lx & 1) + 2 * (ly & 1)) * PS + (ly >> 1) * CXN + (lx >> 1);
+    }
 };
 
 // RN: the last sweeps of a V-cycle also run MgHierarchy::solve's divergence
@@ -115,13 +129,13 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
 {
     constexpr bool RN = MODE == 1, RR = MODE == 2;
     using S = SweepShape<TX, TY, NS, VAR, MODE>;
-    constexpr int H = S::H, RX = S::RX, RY = S::RY, R = S::R;
+    constexpr int H = S::H, RX = S::RX, RY = S::RY, RP = S::RP, PS = S::PS;
     constexpr int P = 4 * NS;
     extern __shared__ double sm[];
     double* xs = sm;
-    double* bs = xs + R;
-    double* iv = bs + R;
-    double* cs = iv + R; // VAR: plane p holds entry d = p < 4 ? p : p + 1
+    double* bs = xs + RP;
+    double* iv = bs + RP;
+    double* cs = iv + RP; // VAR: plane p holds entry d = p < 4 ? p : p + 1
 
     const int nx = A.nx;
     const long long n = (long long)nx * nx;
@@ -136,7 +150,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         const bool rowin = gy >= 0 && gy < nx;
         for (int lx = tx; lx < RX; lx += 32) {
             const int gx = ox + lx;
-            const int l = ly * RX + lx;
+            const int l = S::pidx(lx, ly);
             if (rowin && gx >= 0 && gx < nx) {
                 const long long i = (long long)gy * nx + gx;
                 if (zero_init) xs[l] = 0.0;
@@ -145,7 +159,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 cp_async8(iv + l, inv + i);
                 if (S::CS) {
 #pragma unroll
-                    for (int p = 0; p < 8; ++p) cp_async8(cs + p * R + l, A.coef + (p < 4 ? p : p + 1) * n + i);
+                    for (int p = 0; p < 8; ++p) cp_async8(cs + p * RP + l, A.coef + (p < 4 ? p : p + 1) * n + i);
                 }
             } else {
                 xs[l] = 0.0;
@@ -153,7 +167,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 iv[l] = 0.0;
                 if (S::CS) {
 #pragma unroll
-                    for (int p = 0; p < 8; ++p) cs[p * R + l] = 0.0;
+                    for (int p = 0; p < 8; ++p) cs[p * RP + l] = 0.0;
                 }
             }
         }
@@ -167,7 +181,8 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
             for (int lx = tx; lx < RX; lx += 32) {
                 const int gx = ox + lx;
                 if (gx < 0 || gx >= nx) continue;
-                xs[ly * RX + lx] = xs[ly * RX + lx] + prolong_at2(ec, nxc, gx, gy); // x += P ec
+                const int l = S::pidx(lx, ly);
+                xs[l] = xs[l] + prolong_at2(ec, nxc, gx, gy); // x += P ec
             }
         }
     }
@@ -175,17 +190,16 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
 
     // Fixed node table: thread t owns colour-sub-lattice positions k = t + 256 m
     // of the region (region origin ox, oy is even, so a colour's nodes are
-    // (2 kx + cx, 2 ky + cy) in region coordinates for every pass); shared
-    // offsets and global coordinates are computed once, neighbours are
-    // compile-time offsets from l.
-    constexpr int CXN = RX / 2, CYN = RY / 2, KC = CXN * CYN, KT = (KC + 255) / 256;
+    // (2 kx + cx, 2 ky + cy) in region coordinates for every pass). k is also
+    // the node's index inside its colour plane; the neighbours of a colour-c
+    // node sit at pass-uniform offsets from k in the other planes.
+    constexpr int CXN = S::CXN, KC = S::KC, KT = (KC + 255) / 256;
     static_assert(RX % 2 == 0 && RY % 2 == 0, "even regions keep colour parity");
-    int kl[KT], kx0[KT], ky0[KT];
+    int kx0[KT], ky0[KT];
 #pragma unroll
     for (int m = 0; m < KT; ++m) {
         const int k = threadIdx.x + 256 * m;
         const int ky = k / CXN, kx = k - ky * CXN;
-        kl[m] = 2 * ky * RX + 2 * kx;
         kx0[m] = k < KC ? ox + 2 * kx : -(1 << 30); // out-of-range marker
         ky0[m] = oy + 2 * ky;
     }
@@ -200,24 +214,34 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         const int g = P - 1 - q + (RN ? 1 : 0) + (RR ? 2 : 0);
         const int lox = max(tx0 - g, 0), hix = min(tx0 + TX + g, nx);
         const int loy = max(ty0 - g, 0), hiy = min(ty0 + TY + g, nx);
-        const int lc = cy * RX + cx;
+        const int lc = c * PS;
+        int off[9]; // neighbour d of a colour-c node k: xs[off[d] + k]
+#pragma unroll
+        for (int d = 0; d < 9; ++d) {
+            const int dx = d % 3 - 1, dy = d / 3 - 1;
+            const int ncx = dx ? cx ^ 1 : cx, ncy = dy ? cy ^ 1 : cy;
+            const int sx = dx < 0 ? cx - 1 : (dx > 0 ? cx : 0); // sub-lattice column shift
+            const int sy = dy < 0 ? cy - 1 : (dy > 0 ? cy : 0);
+            off[d] = (ncx + 2 * ncy) * PS + sy * CXN + sx;
+        }
 #pragma unroll
         for (int m = 0; m < KT; ++m) {
             const int gx = kx0[m] + cx, gy = ky0[m] + cy;
             if (gx >= lox && gx < hix && gy >= loy && gy < hiy) {
-                const int l = kl[m] + lc;
+                const int k = threadIdx.x + 256 * m;
+                const int l = lc + k;
                 const double* cp = VAR ? A.coef + ((long long)gy * nx + gx) : nullptr;
                 double s = bs[l];
 #pragma unroll
                 for (int d = 0; d < 9; ++d) {
                     if (d == 4) continue;
                     double a;
-                    if (S::CS) a = cs[(d < 4 ? d : d - 1) * R + l];
+                    if (S::CS) a = cs[(d < 4 ? d : d - 1) * RP + l];
                     else if (VAR) a = A.csplit ? __ldg(A.csplit + (long long)(d < 4 ? d : d - 1) * n + gy * nx +
                                                        ((gx & 1) ? ((nx + 1) >> 1) + (gx >> 1) : (gx >> 1)))
                                                : __ldg(cp + cpo[d]);
                     else a = A.c[d];
-                    s -= a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
+                    s -= a * xs[off[d] + k];
                 }
                 xs[l] = s * iv[l];
             }
@@ -232,7 +256,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         for (int lx = tx; lx < TX; lx += 32) {
             const int gx = tx0 + lx;
             if (gx >= nx) continue;
-            const int l = (ly + H) * RX + lx + H;
+            const int l = S::pidx(lx + H, ly + H);
             const long long i = (long long)gy * nx + gx;
             xout[i] = xs[l];
             if (RN) { // r = b - A x in the reference's row order (op_apply_at)
@@ -241,7 +265,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 for (int d = 0; d < 9; ++d) {
                     double a = VAR ? __ldg(A.coef + cpo[d] + i) : A.c[d];
                     if (d == 4 && A.diag) a += __ldg(A.diag + i);
-                    sum += a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
+                    sum += a * xs[S::pidx(lx + H + (d % 3 - 1), ly + H + (d / 3 - 1))];
                 }
                 const double r = bs[l] - sum;
                 acc += r * r;
@@ -257,23 +281,22 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     if (RR) {
         // fine residual on [tx0, tx0+TX] x [ty0, ty0+TY] (multigrid.cpp:120-121,
         // k_resid_restrict's order), then R = P^T for this tile's coarse nodes
-        double* rs = sm + S::PLANES * R;
+        double* rs = sm + S::PLANES * RP;
         for (int ly = ty; ly <= TY; ly += 8) {
             const int gy = ty0 + ly;
             for (int lx = tx; lx <= TX; lx += 32) {
                 const int gx = tx0 + lx;
                 double r = 0.0;
                 if (gx < nx && gy < nx) {
-                    const int l = (ly + H) * RX + lx + H;
                     const long long i = (long long)gy * nx + gx;
                     double sum = 0.0;
 #pragma unroll
                     for (int d = 0; d < 9; ++d) {
                         double a = VAR ? __ldg(A.coef + cpo[d] + i) : A.c[d];
                         if (d == 4 && A.diag) a += __ldg(A.diag + i);
-                        sum += a * xs[l + (d / 3 - 1) * RX + (d % 3 - 1)];
+                        sum += a * xs[S::pidx(lx + H + (d % 3 - 1), ly + H + (d / 3 - 1))];
                     }
-                    r = bs[l] - sum;
+                    r = bs[S::pidx(lx + H, ly + H)] - sum;
                 }
                 rs[ly * S::RSX + lx] = r;
             }
