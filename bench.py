@@ -509,9 +509,18 @@ def run_ours_c5(args, torch, dist, rank, world, local):
         blk_ms += pr["block"][0]
         blk_n += pr["block"][1]
     peak, peak_src = measured_peak_hbm()
-    blk_bytes = bytes_model.mg_solve_words(c.level) * 8.0 * c.n
+    import ctypes as C
+    from paper_1806_05896_b200 import _lib
+    chain = C.c_int(0)
+    _lib.check(_lib.load().oc_get_tuning(b"heat_chain", C.byref(chain)))
+    # one launch = one substitution direction (c.nt chained block solves), or one block solve
+    per_launch = c.nt if chain.value else 1
+    one_blk_bytes = bytes_model.mg_solve_words(c.level) * 8.0 * c.n
+    blk_bytes = one_blk_bytes * per_launch
     kernel = "k_bottom_cluster<8>"
     traffic = measured_traffic(kernel)
+    if traffic:
+        traffic = dict(traffic, bytes=traffic["bytes"] * per_launch // traffic.get("blocks_per_launch", 1))
     achieved = blk_bytes / (blk_ms / blk_n / 1e3) / 1e9 if blk_n else None
     # one replica alone: IPM time to tolerance and the KKT + P apply bandwidth
     single = solve(0)
@@ -544,20 +553,23 @@ def run_ours_c5(args, torch, dist, rank, world, local):
         "data": "synthetic (seeded sine-mode y_d x exp(-t); no dataset exists for this path)",
         "config": workload(args, world),
         "roofline": {
-            "bound": "hbm", "kernel": f"{kernel} (one heat time-block multigrid solve: 3 "
-                                      "V-cycles on M + tau L + diag(m_k), 65,025 nodes, "
-                                      "one 16-CTA cluster)",
+            "bound": "hbm", "kernel": f"{kernel} ({per_launch} chained heat time-block multigrid "
+                                      "solve(s) per launch, each 3 V-cycles on M + tau L + "
+                                      "diag(m_k), 65,025 nodes; one 16-CTA cluster)",
             "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None,
             "traffic": traffic["bytes"] if traffic else None,
             "traffic_source": traffic["source"] if traffic else None,
             "peak_source": peak_src, "bytes_per_launch": blk_bytes,
             "avg_launch_ms": blk_ms / blk_n if blk_n else None, "launches_in_pass": blk_n,
-            "note": "achieved = SURVEY 8d algorithmic bytes of one block MG solve (287 words "
-                    "per node) / its CUDA-event time on the solver streams in an untimed step "
-                    f"with the same {R} solves in flight; the kernel is latency-bound (256 "
-                    "dependent block solves per preconditioner apply, each on one 16-SM "
-                    "cluster; its data stay on chip after one read), see DESIGN.md",
+            "block_solves_per_launch": per_launch,
+            "avg_block_solve_ms": blk_ms / blk_n / per_launch if blk_n else None,
+            "note": "achieved = SURVEY 8d algorithmic bytes of the launch's block MG solves (287 "
+                    "words per node each) / its CUDA-event time on the solver streams in an "
+                    f"untimed step with the same {R} solves in flight; the kernel is "
+                    "latency-bound (256 dependent block solves per preconditioner apply on one "
+                    "16-SM cluster, at most 7 such clusters resident; its data stay on chip "
+                    "after one read), see DESIGN.md",
         },
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

@@ -458,12 +458,14 @@ int oc_set_tuning(const char* name, int value)
         else if (k == "cluster_bottom") ocb::g_cluster_bottom = value;
         else if (k == "cluster_top8") ocb::g_cluster_top8 = value;
         else if (k == "colour_split") ocb::g_colour_split = value;
+        else if (k == "sweep_lean") ocb::g_sweep_lean = value;
         else if (k == "mgs_persistent") ocb::g_mgs_persistent = value;
         else if (k == "cheb_block") ocb::g_cheb_block = value;
         else if (k == "fuse_norm") ocb::g_fuse_norm = value;
         else if (k == "fuse_restrict") ocb::g_fuse_restrict = value;
         else if (k == "kkt_tiled") ocb::g_kkt_tiled = value;
         else if (k == "heat_fork") ocb::g_heat_fork = value;
+        else if (k == "heat_chain") ocb::g_heat_chain = value;
         else if (k == "lex_start") ocb::g_lex_start = value < 17 ? 17 : value;
         else if (k == "lex_bottom_top") ocb::g_lex_bottom_top = value < 3 ? 3 : (value > 6 ? 6 : value);
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
@@ -483,12 +485,14 @@ int oc_get_tuning(const char* name, int* value)
         else if (k == "cluster_bottom") *value = ocb::g_cluster_bottom;
         else if (k == "cluster_top8") *value = ocb::g_cluster_top8;
         else if (k == "colour_split") *value = ocb::g_colour_split;
+        else if (k == "sweep_lean") *value = ocb::g_sweep_lean;
         else if (k == "mgs_persistent") *value = ocb::g_mgs_persistent;
         else if (k == "cheb_block") *value = ocb::g_cheb_block;
         else if (k == "fuse_norm") *value = ocb::g_fuse_norm;
         else if (k == "fuse_restrict") *value = ocb::g_fuse_restrict;
         else if (k == "kkt_tiled") *value = ocb::g_kkt_tiled;
         else if (k == "heat_fork") *value = ocb::g_heat_fork;
+        else if (k == "heat_chain") *value = ocb::g_heat_chain;
         else if (k == "lex_start") *value = ocb::g_lex_start;
         else if (k == "lex_bottom_top") *value = ocb::g_lex_bottom_top;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);

@@ -437,10 +437,11 @@ __device__ __forceinline__ double op_entry(const Op9& A, int d, long long n, lon
 
 // load a CTA-0 level operator into planar shared memory
 template <int NX>
-__device__ void c0_load(const Op9& A, const C0Level<NX>& L)
+__device__ void c0_load(const Op9& A, const C0Level<NX>& L, long long shift = 0)
 {
     using G = FullG<NX>;
     const long long n = (long long)NX * NX;
+    const double* coef = A.coef ? A.coef + shift : nullptr; // batch element of a chained launch
     for (int i = threadIdx.x; i < G::S; i += blockDim.x) L.x[i] = 0.0; // padding stays zero
     // off-diagonal planes: asynchronous global -> shared copies (all in flight;
     // completed by cp.async.wait_all before the cluster barrier that ends loading)
@@ -453,13 +454,13 @@ __device__ void c0_load(const Op9& A, const C0Level<NX>& L)
             if (A.coef) {
                 const unsigned dst = (unsigned)__cvta_generic_to_shared(L.coef + d * G::S + me);
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
-                             "l"(A.coef + d * n + i)
+                             "l"(coef + d * n + i)
                              : "memory");
             } else {
                 L.coef[d * G::S + me] = A.c[d];
             }
         }
-        const double v = op_entry(A, 4, n, i);
+        const double v = op_entry(A, 4, n, i + shift);
         L.coef[4 * G::S + me] = v;
         L.inv[me] = 1.0 / v;
     }
@@ -501,11 +502,11 @@ struct C0Cycle {
         c0_load<NX>(a.ops[k], L);
         C0Cycle<NX / 2>::load(base + 13 * FullG<NX>::S, a, k + 1);
     }
-    __device__ static void load_top(double* base, const BottomArgs& a, int k) // this level only
+    __device__ static void load_top(double* base, const BottomArgs& a, int k, long long shift = 0) // this level only
     {
         C0Level<NX> L;
         layout(base, L);
-        c0_load<NX>(a.ops[k], L);
+        c0_load<NX>(a.ops[k], L, shift);
     }
     // pre-smoothing, residual and restriction into the next level's b (x zeroed)
     __device__ static void run_pre(double* base, int pre)
@@ -628,8 +629,8 @@ struct Lay {
 
 template <int TOP>
 __global__ void __launch_bounds__(kCT, 1)
-    k_bottom_cluster(BottomArgs a, const double* __restrict__ bg, double* __restrict__ xg,
-                     int cycles, int pre, int post, int check, double* state, int* flags)
+    k_bottom_cluster(BottomArgs a, const double* __restrict__ bg0, double* __restrict__ xg0,
+                     int cycles, int pre, int post, int check, double* state, int* flags, ChainArgs ch)
 {
     using Ly = Lay<TOP>;
     using G8 = typename Ly::G8;
@@ -677,6 +678,18 @@ __global__ void __launch_bounds__(kCT, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
 
+    // A chained launch (heat time blocks, TimeSchurApprox::apply_inverse,
+    // timedep.cpp:268-311) solves ch.nblk batch elements one after the other:
+    // element ob = blk * ch.dbt away from the first, with the right-hand side
+    // b = r + M x_prev formed from the previous element's solution while it is
+    // still in shared memory (own rows and up-to-date halo rows).
+    const int nblk = S8 ? max(ch.nblk, 1) : 1;
+#pragma unroll 1
+    for (int blk = 0; blk < nblk; ++blk) {
+    const long long ob = S8 ? (long long)blk * ch.dbt : 0; // batch element offset
+    const double* __restrict__ bg = bg0 + ob * ch.ns;
+    double* __restrict__ xg = xg0 + ob * ch.ns;
+    const double* diag8 = (S8 && a.ops[0].diag) ? a.ops[0].diag + ob * ch.ns : nullptr;
     // ---- load. Level 8: b and 1/a_ii of the thread's 16 nodes in registers.
     double rb8[S8 ? G8::NPT : 1][4] = {}, ri8[S8 ? G8::NPT : 1][4] = {};
     if constexpr (S8) {
@@ -688,10 +701,19 @@ __global__ void __launch_bounds__(kCT, 1)
                 rb8[m][c] = ri8[m][c] = 0.0;
                 if (o8.valid(m, c)) {
                     const long long gi = (long long)o8.gy(m, c) * G8::NX + o8.gx(m, c);
-                    rb8[m][c] = bg[gi];
-                    ri8[m][c] = 1.0 / (A.c[4] + (A.diag ? A.diag[gi] : 0.0)); // = k_inv_diag
+                    double bv = bg[gi];
+                    if (blk > 0) { // + M x_prev in op_apply_at's order (k_rhs_plus_mass)
+                        double sm9 = 0.0;
+#pragma unroll
+                        for (int d = 0; d < 9; ++d)
+                            sm9 += ch.mc[d] * x8[o8.q[m] + G8::nb(c, d % 3 - 1, d / 3 - 1)];
+                        bv = bv + sm9;
+                    }
+                    rb8[m][c] = bv;
+                    ri8[m][c] = 1.0 / (A.c[4] + (diag8 ? diag8[gi] : 0.0)); // = k_inv_diag
                 }
             }
+        if (blk > 0) __syncthreads(); // every read of the previous solution is done
         for (int i = threadIdx.x; i < G8::XS; i += blockDim.x) x8[i] = 0.0;
     }
     // the G0 level's four nodes per thread: coefficients, 1/a_ii, b in registers
@@ -699,12 +721,13 @@ __global__ void __launch_bounds__(kCT, 1)
     {
         const Op9& A = a.ops[K0];
         const long long n = (long long)NX0 * NX0;
+        const long long sh = ob * 9 * n;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             if (o0.valid(c)) {
                 const long long gi = (long long)o0.gy(c) * NX0 + o0.gx(c);
 #pragma unroll
-                for (int d = 0; d < 9; ++d) ra[c][d] = op_entry(A, d, n, gi);
+                for (int d = 0; d < 9; ++d) ra[c][d] = op_entry(A, d, n, gi + sh);
                 rinv[c] = 1.0 / ra[c][4];
                 rb[c] = S8 ? 0.0 : bg[gi];
             } else {
@@ -718,13 +741,14 @@ __global__ void __launch_bounds__(kCT, 1)
     if constexpr (Ly::S1) {
         const Op9& A = a.ops[K0 + 1];
         const long long n = (long long)G1::NX * G1::NX;
+        const long long sh = ob * 9 * n;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             if (o1.valid(c)) {
                 const long long gi = (long long)o1.gy(c) * G1::NX + o1.gx(c);
 #pragma unroll
                 for (int d = 0; d < 9; ++d) {
-                    const double v = op_entry(A, d, n, gi);
+                    const double v = op_entry(A, d, n, gi + sh);
                     c1[(c * 9 + d) * G1::GROUP + threadIdx.x] = v;
                     if (d == 4) i1[o1.slot(c)] = 1.0 / v;
                 }
@@ -740,14 +764,14 @@ __global__ void __launch_bounds__(kCT, 1)
     // operator (k_coarse_op) where CTA 0 keeps level 5
     double* cops = c0base;
     if (w > 0) {
-        const double* src = a.cop + (size_t)kCopRows * kCopN * (w - 1);
+        const double* src = a.cop + ob * kCopN * kCopN + (size_t)kCopRows * kCopN * (w - 1);
         for (int i = threadIdx.x; i < kCopRows * kCopN; i += blockDim.x) {
             const unsigned dst = (unsigned)__cvta_generic_to_shared(cops + i);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src + i) : "memory");
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     } else {
-        C0Cycle<NC>::load_top(c0base, a, K0 + (Ly::S1 ? 2 : 1));
+        C0Cycle<NC>::load_top(c0base, a, K0 + (Ly::S1 ? 2 : 1), ob * 9 * NC * NC);
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     }
     cl.sync();
@@ -826,7 +850,7 @@ __global__ void __launch_bounds__(kCT, 1)
 #pragma unroll
                 for (int d = 0; d < 9; ++d) {
                     double av = A.c[d];
-                    if (d == 4 && A.diag) av += A.diag[gi];
+                    if (d == 4 && diag8) av += diag8[gi];
                     s += av * x8[o8.q[m] + G8::nb(c, d % 3 - 1, d / 3 - 1)];
                 }
                 const double r = rb8[m][c] - s;
@@ -1040,7 +1064,8 @@ __global__ void __launch_bounds__(kCT, 1)
             if (o0.valid(c)) xg[(long long)o0.gy(c) * NX0 + o0.gx(c)] = x0[o0.me(c)];
     }
     if (check && state && w == 0 && threadIdx.x == 0) state[0] = prev;
-    cl.sync(); // no CTA exits while a neighbour may still address its shared memory
+    cl.sync(); // no CTA exits (or reloads) while a neighbour may still address its shared memory
+    } // chained batch elements
 }
 
 template <int TOP>
@@ -1071,7 +1096,7 @@ bool set_attrs()
 
 template <int TOP>
 void launch_top(cudaStream_t s, const BottomArgs& a, const double* b, double* x, int cycles,
-                int pre, int post, bool check, double* state, int* flags)
+                int pre, int post, bool check, double* state, int* flags, const ChainArgs& ch)
 {
     static const bool attr = set_attrs<TOP>();
     (void)attr;
@@ -1079,7 +1104,7 @@ void launch_top(cudaStream_t s, const BottomArgs& a, const double* b, double* x,
     cudaLaunchConfig_t cfg = cluster_cfg<TOP>(s, &at);
     note_launch();
     cudaLaunchKernelEx(&cfg, k_bottom_cluster<TOP>, a, b, x, cycles, pre, post, check ? 1 : 0,
-                       state, flags);
+                       state, flags, ch);
 }
 
 static_assert(Lay<7>::total() * sizeof(double) <= 220 * 1024, "cluster layout exceeds shared memory");
@@ -1167,11 +1192,22 @@ void launch_coarse_op(cudaStream_t s, const BottomArgs& a, int batch, int pre, i
 void launch_bottom_cluster(cudaStream_t s, const ClusterArgs& a, const double* b, double* x,
                            int cycles, int pre, int post, bool check, double* state, int* flags)
 {
+    ChainArgs one{};
+    one.nblk = 1;
     if (a.ops[0].nx == 255 && !a.ops[0].coef)
-        launch_top<8>(s, a, b, x, cycles, pre, post, check, state, flags);
-    else if (a.ops[0].nx == 127) launch_top<7>(s, a, b, x, cycles, pre, post, check, state, flags);
-    else if (a.ops[0].nx == 63) launch_top<6>(s, a, b, x, cycles, pre, post, check, state, flags);
+        launch_top<8>(s, a, b, x, cycles, pre, post, check, state, flags, one);
+    else if (a.ops[0].nx == 127) launch_top<7>(s, a, b, x, cycles, pre, post, check, state, flags, one);
+    else if (a.ops[0].nx == 63) launch_top<6>(s, a, b, x, cycles, pre, post, check, state, flags, one);
     else throw std::runtime_error("cluster bottom: top level must be 6, 7 or a constant-stencil 8");
+}
+
+void launch_cluster_chain(cudaStream_t s, const ClusterArgs& a, const double* r, double* x,
+                          const ChainArgs& ch, int cycles, int pre, int post, bool check,
+                          double* state, int* flags)
+{
+    if (!(a.ops[0].nx == 255 && !a.ops[0].coef))
+        throw std::runtime_error("cluster chain: a constant-stencil level-8 hierarchy expected");
+    launch_top<8>(s, a, r, x, cycles, pre, post, check, state, flags, ch);
 }
 
 } // namespace ocb

@@ -17,6 +17,8 @@
 
 namespace ocb {
 
+std::atomic<int> g_sweep_lean{0}; // tuning: operands of variable sweeps read in the passes (see SweepShape)
+
 namespace {
 
 __device__ __forceinline__ void cp_async8(void* dst_smem, const void* src)
@@ -73,7 +75,10 @@ __device__ __forceinline__ double prolong_at2(const double* __restrict__ ec, int
 // MODE 0: plain; 1: + divergence check (one more updated ring); 2: + residual
 // and restriction (two more updated rings). Extra rings are staged in pairs so
 // the region origin stays even.
-template <int TX, int TY, int NS, bool VAR, int MODE = 0>
+// LEAN (variable operators read through L1 only): 1 = 1/a_ii, 2 = 1/a_ii and b are
+// read from global memory in the passes instead of being staged (smaller
+// footprint, more CTAs per SM: the passes are load-latency bound).
+template <int TX, int TY, int NS, bool VAR, int MODE = 0, int LEAN_ = 0>
 struct SweepShape {
     static constexpr int H = 4 * NS + (MODE ? 2 : 0);
     static constexpr int RX = TX + 2 * H, RY = TY + 2 * H;
@@ -91,7 +96,8 @@ struct SweepShape {
     // fit (coalesced row copies, read once per launch for all fused sweeps);
     // otherwise read through L1 (colour-strided, L2-bandwidth bound)
     static constexpr bool CS = VAR && (size_t)11 * RP * sizeof(double) <= 100 * 1024; // >= 2 CTAs/SM
-    static constexpr int PLANES = CS ? 11 : 3; // x, b, inv (+ 8 off-diagonals)
+    static constexpr int LEAN = (VAR && !CS) ? LEAN_ : 0;
+    static constexpr int PLANES = CS ? 11 : 3 - LEAN; // x, b, inv (+ 8 off-diagonals)
     static constexpr int RSX = TX + 1, RSN = (TX + 1) * (TY + 1); // MODE 2: fine residual rows
     static constexpr size_t smem = ((size_t)PLANES * RP + (MODE == 2 ? RSN : 0)) * sizeof(double);
     // planar index of region node (lx, ly)
@@ -119,7 +125,7 @@ struct RestrictOut {
     double* xc;
 };
 
-template <int TX, int TY, int NS, bool VAR, int MODE = 0>
+template <int TX, int TY, int NS, bool VAR, int MODE = 0, int LEAN_ = 0>
 __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__ b,
                                                const double* __restrict__ inv,
                                                const double* __restrict__ xin,
@@ -128,8 +134,8 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                                                int zero_init, NormCheck nc, RestrictOut ro)
 {
     constexpr bool RN = MODE == 1, RR = MODE == 2;
-    using S = SweepShape<TX, TY, NS, VAR, MODE>;
-    constexpr int H = S::H, RX = S::RX, RY = S::RY, RP = S::RP, PS = S::PS;
+    using S = SweepShape<TX, TY, NS, VAR, MODE, LEAN_>;
+    constexpr int H = S::H, RX = S::RX, RY = S::RY, RP = S::RP, PS = S::PS, LEAN = S::LEAN;
     constexpr int P = 4 * NS;
     extern __shared__ double sm[];
     double* xs = sm;
@@ -155,16 +161,16 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 const long long i = (long long)gy * nx + gx;
                 if (zero_init) xs[l] = 0.0;
                 else cp_async8(xs + l, xin + i);
-                cp_async8(bs + l, b + i);
-                cp_async8(iv + l, inv + i);
+                if (LEAN < 2) cp_async8(bs + l, b + i);
+                if (LEAN < 1) cp_async8(iv + l, inv + i);
                 if (S::CS) {
 #pragma unroll
                     for (int p = 0; p < 8; ++p) cp_async8(cs + p * RP + l, A.coef + (p < 4 ? p : p + 1) * n + i);
                 }
             } else {
                 xs[l] = 0.0;
-                bs[l] = 0.0;
-                iv[l] = 0.0;
+                if (LEAN < 2) bs[l] = 0.0;
+                if (LEAN < 1) iv[l] = 0.0;
                 if (S::CS) {
 #pragma unroll
                     for (int p = 0; p < 8; ++p) cs[p * RP + l] = 0.0;
@@ -231,7 +237,9 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 const int k = threadIdx.x + 256 * m;
                 const int l = lc + k;
                 const double* cp = VAR ? A.coef + ((long long)gy * nx + gx) : nullptr;
-                double s = bs[l];
+                const long long gi = (long long)gy * nx + gx;
+                double s = LEAN == 2 ? __ldg(b + gi) : bs[l];
+                const double ivl = LEAN >= 1 ? __ldg(inv + gi) : iv[l];
 #pragma unroll
                 for (int d = 0; d < 9; ++d) {
                     if (d == 4) continue;
@@ -243,7 +251,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                     else a = A.c[d];
                     s -= a * xs[off[d] + k];
                 }
-                xs[l] = s * iv[l];
+                xs[l] = s * ivl;
             }
         }
         __syncthreads();
@@ -267,7 +275,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                     if (d == 4 && A.diag) a += __ldg(A.diag + i);
                     sum += a * xs[S::pidx(lx + H + (d % 3 - 1), ly + H + (d / 3 - 1))];
                 }
-                const double r = bs[l] - sum;
+                const double r = (LEAN == 2 ? __ldg(b + i) : bs[l]) - sum;
                 acc += r * r;
             }
         }
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                         if (d == 4 && A.diag) a += __ldg(A.diag + i);
                         sum += a * xs[S::pidx(lx + H + (d % 3 - 1), ly + H + (d / 3 - 1))];
                     }
-                    r = bs[S::pidx(lx + H, ly + H)] - sum;
+                    r = (LEAN == 2 ? __ldg(b + i) : bs[S::pidx(lx + H, ly + H)]) - sum;
                 }
                 rs[ly * S::RSX + lx] = r;
             }
@@ -444,22 +452,35 @@ __global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long 
     if (dfull) dfull[bt * n + i] = a;
 }
 
-template <int TX, int TY, int NS, bool VAR, int MODE>
-void sweep_go_mode(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
+template <int TX, int TY, int NS, bool VAR, int MODE, int LEAN = 0>
+void sweep_go_lean(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
                    double* xo, bool forward, bool zero_init, const double* ec, const NormCheck& nc,
                    const RestrictOut& ro)
 {
-    constexpr size_t smem = SweepShape<TX, TY, NS, VAR, MODE>::smem;
+    constexpr size_t smem = SweepShape<TX, TY, NS, VAR, MODE, LEAN>::smem;
     static const bool attr = [] { // thread-safe one-time setup
-        cudaFuncSetAttribute(k_sweep<TX, TY, NS, VAR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_sweep<TX, TY, NS, VAR, MODE, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         return true;
     }();
     (void)attr;
     dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
     note_launch();
-    k_sweep<TX, TY, NS, VAR, MODE><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
-                                                            zero_init ? 1 : 0, nc, ro);
+    k_sweep<TX, TY, NS, VAR, MODE, LEAN><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
+                                                                  zero_init ? 1 : 0, nc, ro);
+}
+
+template <int TX, int TY, int NS, bool VAR, int MODE>
+void sweep_go_mode(cudaStream_t s, const Op9& A, const double* b, const double* inv, const double* x,
+                   double* xo, bool forward, bool zero_init, const double* ec, const NormCheck& nc,
+                   const RestrictOut& ro)
+{
+    if constexpr (VAR && !SweepShape<TX, TY, NS, VAR, MODE>::CS && NS <= 2) {
+        const int lean = g_sweep_lean.load();
+        if (lean == 1) return sweep_go_lean<TX, TY, NS, VAR, MODE, 1>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
+        if (lean == 2) return sweep_go_lean<TX, TY, NS, VAR, MODE, 2>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
+    }
+    sweep_go_lean<TX, TY, NS, VAR, MODE, 0>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
 }
 
 // the fused variants only for the 1- and 2-sweep launches that end a phase

@@ -565,6 +565,7 @@ void launch_kkt(cudaStream_t s, const ProbDev& P, const double* ty, const double
 std::atomic<int> g_cheb_block{1};
 std::atomic<int> g_kkt_tiled{1};
 std::atomic<int> g_heat_fork{1};
+std::atomic<int> g_heat_chain{1};
 std::atomic<long long> g_tuning_gen{0};
 
 void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const double* e,

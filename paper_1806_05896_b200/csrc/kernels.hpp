@@ -58,6 +58,7 @@ void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long 
                      long long fds, double* dfull = nullptr);
 // colour-split copy (Op9::csplit) of a variable operator's 8 off-diagonal planes
 extern std::atomic<int> g_mgs_persistent; // GMRES columns j+1 >= this use the persistent MGS launch (0: never)
+extern std::atomic<int> g_sweep_lean;   // variable tiled sweeps: 1 = 1/a_ii, 2 = 1/a_ii and b read in the passes, not staged
 extern std::atomic<int> g_colour_split; // 1: the fine level of >= 1023^2 hierarchies sweeps from it
 void launch_colour_split(cudaStream_t s, int nx, const double* coef, double* out);
 void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, const double* x,
@@ -120,6 +121,22 @@ void cluster_probes(int enable, unsigned long long* out64);
 void lex_probes(int enable, unsigned long long* out512); // lexicographic sweep stamps
 void launch_bottom_cluster(cudaStream_t s, const ClusterArgs& a, const double* b, double* x,
                            int cycles, int pre, int post, bool check, double* state, int* flags);
+// Chained level-8 solves in ONE launch (the heat time-block substitution,
+// timedep.cpp:268-311): batch elements first, first + dbt, ... (nblk of them;
+// `a`, r and x address the first). Element j > 0 solves A_j x_j = r_j + M x_{j-1}
+// with M the constant 9-point stencil mc (k_rhs_plus_mass's arithmetic), x_{j-1}
+// taken from shared memory. ns = nodes per element (stride of r, x and the
+// fine diagonal; coarse operators, LU and dense operator are batch-contiguous).
+struct ChainArgs {
+    int nblk;
+    int dbt;
+    long long ns;
+    double mc[9];
+};
+void launch_cluster_chain(cudaStream_t s, const ClusterArgs& a, const double* r, double* x,
+                          const ChainArgs& ch, int cycles, int pre, int post, bool check,
+                          double* state, int* flags);
+extern std::atomic<int> g_heat_chain; // 1: a heat substitution direction is one chained cluster launch
 // Dense operator of the V-cycle below level 5 (levels 4, 3 and the level-2 LU)
 // for the cluster kernel: a.ops[0] = level 4, a.ops[1] = level 3 of batch
 // element 0 (elements are 9 n_k apart), lu/perm of element 0; out: batch x 225 x 225.

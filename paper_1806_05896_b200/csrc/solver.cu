@@ -501,6 +501,29 @@ void Hierarchy::solve(Ctx& c, const double* b, double* x, const MgParams& p, int
     launch_check("multigrid solve");
 }
 
+bool Hierarchy::can_chain(const MgParams& p, const Op9& M) const
+{
+    return kb_ == 0 && cluster_ && !lex_ && g_heat_chain.load() && p.cycles > 0 && !M.coef &&
+           !M.diag && nx_[0] == 255 && !fine_.coef && fine_.diag && fine_diag_stride_ == level_n(0);
+}
+
+bool Hierarchy::solve_chain(Ctx& c, const double* r, double* x, const MgParams& p, int first,
+                            int step, int count, const Op9& M, int* flags)
+{
+    if (!can_chain(p, M) || count <= 0) return false;
+    ensure_coarse_op(c, p.pre, p.post);
+    ChainArgs ch{};
+    ch.nblk = count;
+    ch.dbt = step;
+    ch.ns = level_n(0);
+    for (int d = 0; d < 9; ++d) ch.mc[d] = M.c[d];
+    const long long off = (long long)first * ch.ns;
+    launch_cluster_chain(c.stream, bottom_args(0, first), r + off, x + off, ch, p.cycles, p.pre,
+                         p.post, true, state_.get(), flags);
+    launch_check("multigrid chained solve");
+    return true;
+}
+
 void Hierarchy::smooth(Ctx& c, const double* b, double* x, bool forward, int bt)
 {
     const Op9 A = level_op(0, bt);
@@ -929,6 +952,18 @@ void Problem::time_schur(const double* r, double* out)
 {
     // TimeSchurApprox::apply_inverse (timedep.cpp:268-311)
     int* fl = flags_.get();
+    if (Hheat_.can_chain(mg_, P.M)) {
+        // each substitution direction as one chained cluster launch (the cluster
+        // keeps its SMs for all nt blocks; right-hand sides formed on chip)
+        {
+            ProfScope ps(ctx, kProfBlock);
+            Hheat_.solve_chain(ctx, r, tf_.get(), mg_, 0, 1, nt_, P.M, fl);
+        }
+        launch_schur_middle(ctx.stream, P, nullptr, tf_.get(), t3_.get());
+        ProfScope ps(ctx, kProfBlock);
+        Hheat_.solve_chain(ctx, t3_.get(), out, mg_, nt_ - 1, -1, nt_, P.M, fl);
+        return;
+    }
     for (int k = 0; k < nt_; ++k) {
         const long long off = (long long)k * ns_;
         launch_rhs_plus_mass(ctx.stream, P, r + off, k > 0 ? tf_.get() + off - ns_ : nullptr,

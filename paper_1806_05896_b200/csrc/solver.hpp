@@ -160,6 +160,13 @@ public:
     void build_rediscretized(Ctx& c, const Op9& fine, const std::vector<const double*>& base);
     // solve: `cycles` V-cycles from x = 0 with the divergence check.
     void solve(Ctx& c, const double* b, double* x, const MgParams& p, int bt, int* flags);
+    // the heat substitution in one chained cluster launch: batch elements
+    // first, first + step, ... (count of them), element j solving
+    // A_j x_j = r_j + M x_{j-1}; r and x are whole space-time vectors.
+    // Returns false (nothing launched) when this hierarchy cannot chain.
+    bool can_chain(const MgParams& p, const Op9& M) const;
+    bool solve_chain(Ctx& c, const double* r, double* x, const MgParams& p, int first, int step,
+                     int count, const Op9& M, int* flags);
     // one smoothing sweep on the fine level (in place through the scratch buffer)
     void smooth(Ctx& c, const double* b, double* x, bool forward, int bt);
     // cluster bottom: (re)compute the dense levels <= 4 cycle operator for these
