@@ -261,6 +261,148 @@ __global__ void __launch_bounds__(kT) k_kkt_heat(ProbDev P, const double* __rest
     }
 }
 
+// ------------------------------------------------------------ KKT (heat), tiled
+// The same operator and arithmetic as k_kkt_heat (every stencil sum in the
+// reference's entry order, one FMA per entry), staged through shared memory:
+// a CTA handles one 32 x 16 node tile of one time block k. y_k, y_{k-1}, p_k,
+// p_{k+1} and the difference w_k - v_k of the tile plus a one-node halo are
+// loaded once with coalesced row loads (0 outside the grid and for the absent
+// neighbour blocks: fma(a, 0, s) = s, and the k-edge terms are skipped as in
+// k_kkt_heat), instead of 54 loads per node through L1. A thread owns two
+// vertically adjacent nodes and reads each field's 4 x 3 window once (30
+// shared loads per node). Tiles are numbered time-fastest, so the CTAs that
+// share y_k / p_k tiles run together and the re-read hits L2. RESID: the
+// fixed grid of kRedBlocks CTAs walks the tiles in a fixed order
+// (deterministic partials of |b - A x|^2).
+template <bool HAS_TY, bool RESID>
+__global__ void __launch_bounds__(256) k_kkt_heat_tiled(ProbDev P, const double* __restrict__ ty,
+                                                        const double* __restrict__ tw,
+                                                        const double* __restrict__ tv,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ out,
+                                                        const double* __restrict__ b,
+                                                        double* __restrict__ part)
+{
+    constexpr int T = kKV * kKH;
+    __shared__ double sf[5 * T]; // y_k, y_{k-1}, p_k, p_{k+1}, w_k - v_k
+    __shared__ double sh[32];
+    const int nx = P.nx, nt = P.nt;
+    const long long ns = P.ns, N = P.ny;
+    const double* y = x;
+    const double* w = x + N;
+    const double* v = x + 2 * N;
+    const double* p = x + 3 * N;
+    const int tilesx = (nx + kKX - 1) / kKX, tilesy = (nx + kKY - 1) / kKY;
+    const long long ntiles = (long long)tilesx * tilesy * nt;
+    const int tx = threadIdx.x & 31, tyy = threadIdx.x >> 5; // 8 warps
+    double acc = 0.0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int k = (int)(t % nt);
+        const int ts = (int)(t / nt);
+        const int x0 = (ts % tilesx) * kKX, y0 = (ts / tilesx) * kKY;
+        const long long off = (long long)k * ns;
+        const bool hm = k > 0, hp = k + 1 < nt;
+        __syncthreads(); // the previous tile's readers are done
+        for (int r = tyy; r < kKV; r += 8) {
+            const int gy = y0 + r - 1;
+            const bool rok = gy >= 0 && gy < nx;
+#pragma unroll
+            for (int c0 = 0; c0 < kKH; c0 += 32) {
+                const int c = c0 + tx;
+                if (c < kKH) {
+                    const int gx = x0 + c - 1;
+                    const bool ok = rok && gx >= 0 && gx < nx;
+                    const long long i = ok ? off + (long long)gy * nx + gx : 0;
+                    const int l = r * kKH + c;
+                    sf[l] = ok ? __ldg(y + i) : 0.0;
+                    sf[T + l] = (ok && hm) ? __ldg(y + i - ns) : 0.0;
+                    sf[2 * T + l] = ok ? __ldg(p + i) : 0.0;
+                    sf[3 * T + l] = (ok && hp) ? __ldg(p + i + ns) : 0.0;
+                    sf[4 * T + l] = ok ? __ldcs(w + i) - __ldcs(v + i) : 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        const int gx = x0 + tx;
+        const int ly = 2 * tyy; // rows ly, ly + 1 of the tile
+        if (gx < nx && y0 + ly < nx) {
+            // stencil sums of the two nodes from a field's 4 x 3 window, in
+            // op_apply_at's entry order (d = 0..8, one FMA per entry)
+            double My[2], Mly[2], Mym[2], Mp[2], Mlp[2], Mpp[2], Mwv[2];
+            auto window = [&](const double* f, double (&q)[12]) {
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) q[rr * 3 + cc] = f[(ly + rr) * kKH + tx + cc];
+            };
+            auto sum9 = [&](const double (&c)[9], const double (&q)[12], int h) {
+                double a = 0.0;
+#pragma unroll
+                for (int d = 0; d < 9; ++d) a += c[d] * q[h * 3 + d];
+                return a;
+            };
+            {
+                double q[12];
+                window(sf, q);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    My[h] = sum9(P.M.c, q, h);
+                    Mly[h] = sum9(P.Mtl.c, q, h);
+                }
+                window(sf + T, q);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) Mym[h] = sum9(P.M.c, q, h);
+                window(sf + 2 * T, q);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    Mlp[h] = sum9(P.Mtl.c, q, h);
+                    Mp[h] = sum9(P.M.c, q, h);
+                }
+                window(sf + 3 * T, q);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) Mpp[h] = sum9(P.M.c, q, h);
+                window(sf + 4 * T, q);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) Mwv[h] = sum9(P.M.c, q, h);
+            }
+            const double sk = P.tau * P.qw[k];
+            const double ak = P.alpha * P.tau * P.qw[k];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int gy = y0 + ly + h;
+                if (gy >= nx) continue;
+                const long long g = off + (long long)gy * nx + gx;
+                const double hy = sk * My[h];
+                double ktp = Mlp[h];
+                if (hp) ktp -= Mpp[h];
+                double ky = Mly[h];
+                if (hm) ky -= Mym[h];
+                double ry = hy;
+                if (HAS_TY) ry += ty[g] * sf[(ly + h + 1) * kKH + tx + 1];
+                ry = ry + ktp;
+                const double rw = (ak * Mwv[h] + tw[g] * __ldcs(w + g)) - P.tau * Mp[h];
+                const double rv = ((-ak) * Mwv[h] + tv[g] * __ldcs(v + g)) + P.tau * Mp[h];
+                const double rp = ky - P.tau * Mwv[h];
+                if (RESID) {
+                    const double d0 = b[g] - ry, d1 = b[N + g] - rw, d2 = b[2 * N + g] - rv,
+                                 d3 = b[3 * N + g] - rp;
+                    acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+                }
+                if (out) {
+                    __stcs(out + g, ry);
+                    __stcs(out + N + g, rw);
+                    __stcs(out + 2 * N + g, rv);
+                    __stcs(out + 3 * N + g, rp);
+                }
+            }
+        }
+    }
+    if (RESID) {
+        acc = block_sum(acc, sh);
+        if (threadIdx.x == 0) part[blockIdx.x] = acc;
+    }
+}
+
 // ------------------------------------------------------------------- Chebyshev
 // ChebyshevSemiIteration (chebyshev.cpp:9-75) on s_k M + diag(e), Jacobi
 // scaled with the fixed interval [1/4, 9/4]: omega = 0.8, rho = 0.8.
@@ -312,73 +454,111 @@ struct ChebSteps {
     int st0, nst; // first step index (>= 2) and steps in this launch
 };
 
-__global__ void __launch_bounds__(256) k_cheb_block(ProbDev P, const double* __restrict__ e, double omega,
+// Thread mapping: thread t owns the kChebSeg vertically consecutive region
+// nodes of column t % R in row segment t / R, so one 3-column window of
+// kChebSeg + 2 rows serves all its stencil sums of a step (27 shared loads for
+// 7 nodes instead of 63), and its nodes' g, e and 1/d stay in registers for
+// all steps (d as k_cheb_step forms it; no division per step). Only the two
+// iterates live in shared memory (one zero row above and below the region).
+constexpr int kChebSeg = 7;
+static_assert(kChebR % kChebSeg == 0 && (kChebR / kChebSeg) * kChebR <= 256, "column segments cover the region");
+
+__global__ void __launch_bounds__(256, 3) k_cheb_block(ProbDev P, const double* __restrict__ e, double omega,
                                                     ChebSteps S, const double* __restrict__ prev,
                                                     const double* __restrict__ cur,
                                                     const double* __restrict__ gv,
                                                     double* __restrict__ out_prev,
                                                     double* __restrict__ out_cur)
 {
-    constexpr int R = kChebR, RR = R * R;
+    constexpr int R = kChebR, RA = (R + 2) * R, SEG = kChebSeg;
     extern __shared__ double csm[];
-    double* yp = csm;
-    double* yc = yp + RR;
-    double* gs = yc + RR;
-    double* es = gs + RR;
+    double* pa = csm + R;      // previous iterate (row -1 and row R are zero rows)
+    double* pc = pa + RA;      // current iterate
     const int nx = P.nx, k = blockIdx.z;
     const long long off = (long long)k * P.ns;
     const int tx0 = blockIdx.x * kChebT, ty0 = blockIdx.y * kChebT;
     const int ox = tx0 - kChebTS, oy = ty0 - kChebTS;
-    for (int l = threadIdx.x; l < RR; l += blockDim.x) {
-        const int gy = oy + l / R, gx = ox + l % R;
-        double a = 0.0, c = 0.0, gg = 0.0, ee = 0.0;
-        if (gx >= 0 && gx < nx && gy >= 0 && gy < nx) {
-            const long long g = off + (long long)gy * nx + gx;
-            a = prev ? prev[g] : 0.0;
-            c = cur[g];
-            gg = gv[g];
-            ee = e ? e[g] : 0.0;
+    const int cx = threadIdx.x % R, r0 = (threadIdx.x / R) * SEG;
+    const bool own = threadIdx.x < (R / SEG) * R;
+    const int gx = ox + cx;
+    for (int l = threadIdx.x; l < R; l += blockDim.x) { // zero rows
+        csm[l] = 0.0;
+        csm[RA + l] = 0.0;
+        csm[(R + 1) * R + l] = 0.0;
+        csm[RA + (R + 1) * R + l] = 0.0;
+    }
+    const double sk = P.heat ? P.tau * P.qw[k] : 1.0;
+    double gr[SEG], er[SEG], idr[SEG];
+    bool in[SEG];
+    if (own) {
+#pragma unroll
+        for (int m = 0; m < SEG; ++m) {
+            const int gy = oy + r0 + m;
+            in[m] = gx >= 0 && gx < nx && gy >= 0 && gy < nx;
+            double a = 0.0, c = 0.0;
+            gr[m] = er[m] = 0.0;
+            if (in[m]) {
+                const long long g = off + (long long)gy * nx + gx;
+                a = prev ? prev[g] : 0.0;
+                c = cur[g];
+                gr[m] = gv[g];
+                er[m] = e ? e[g] : 0.0;
+            }
+            idr[m] = 1.0 / (sk * P.M.c[4] + (e ? er[m] : 0.0));
+            pa[(r0 + m) * R + cx] = a;
+            pc[(r0 + m) * R + cx] = c;
         }
-        yp[l] = a;
-        yc[l] = c;
-        gs[l] = gg;
-        es[l] = ee;
     }
     __syncthreads();
-    const double sk = P.heat ? P.tau * P.qw[k] : 1.0;
-    double* pa = yp;
-    double* pc = yc;
     for (int i = 0; i < S.nst; ++i) {
         const int st = S.st0 + i;
         const double wk = S.wk[i];
         const int lo = i + 1, hi = R - i - 1; // region rows/columns still exact after this step
-        for (int l = threadIdx.x; l < RR; l += blockDim.x) {
-            const int ly = l / R, lx = l - ly * R;
-            const int gy = oy + ly, gx = ox + lx;
-            if (ly < lo || ly >= hi || lx < lo || lx >= hi || gx < 0 || gx >= nx || gy < 0 || gy >= nx) continue;
-            double az = 0.0;
+        if (own && cx >= lo && cx < hi) {
+            // rolling window: rows r0+m-1 .. r0+m+1, columns cx-1 .. cx+1 of the current iterate
+            double q[9];
 #pragma unroll
-            for (int d = 0; d < 9; ++d) az += P.M.c[d] * pc[l + (d / 3 - 1) * R + (d % 3 - 1)];
-            if (P.heat) az = (P.tau * P.qw[k]) * az;
-            if (e) az += es[l] * pc[l];
-            const double invd = 1.0 / (sk * P.M.c[4] + (e ? es[l] : 0.0));
-            const double s_cur = pc[l] - omega * invd * az;
-            const double pv = st == 2 ? 0.0 : pa[l];
-            pa[l] = wk * (s_cur + gs[l] - pv) + pv;
+            for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) q[(rr + 1) * 3 + cc] = pc[(r0 + rr - 1) * R + cx + cc - 1];
+#pragma unroll
+            for (int m = 0; m < SEG; ++m) {
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    q[cc] = q[3 + cc];
+                    q[3 + cc] = q[6 + cc];
+                    q[6 + cc] = pc[(r0 + m + 1) * R + cx + cc - 1];
+                }
+                const int ly = r0 + m;
+                if (ly < lo || ly >= hi || !in[m]) continue;
+                // k_cheb_step's expressions with the contractions it compiles to
+                // spelled out (the hoisted omega / d product must not change them)
+                double az = 0.0;
+#pragma unroll
+                for (int d = 0; d < 9; ++d) az = __fma_rn(P.M.c[d], q[d], az);
+                if (P.heat) az = __dmul_rn(__dmul_rn(P.tau, P.qw[k]), az);
+                const double pcl = q[4];
+                if (e) az = __fma_rn(er[m], pcl, az);
+                const double s_cur = __fma_rn(az, __dmul_rn(omega, -idr[m]), pcl);
+                const int l = ly * R + cx;
+                const double pv = st == 2 ? 0.0 : pa[l];
+                pa[l] = __fma_rn(wk, __dsub_rn(__dadd_rn(s_cur, gr[m]), pv), pv);
+            }
         }
         __syncthreads();
         double* t = pa;
         pa = pc;
         pc = t;
     }
-    for (int l = threadIdx.x; l < kChebT * kChebT; l += blockDim.x) {
-        const int ly = l / kChebT, lx = l - ly * kChebT;
-        const int gy = ty0 + ly, gx = tx0 + lx;
-        if (gx >= nx || gy >= nx) continue;
-        const long long g = off + (long long)gy * nx + gx;
-        const int q = (ly + kChebTS) * R + lx + kChebTS;
-        if (out_prev) out_prev[g] = pa[q];
-        out_cur[g] = pc[q];
+    if (own && cx >= kChebTS && cx < kChebTS + kChebT && gx < nx) {
+#pragma unroll
+        for (int m = 0; m < SEG; ++m) {
+            const int ly = r0 + m, gy = oy + ly;
+            if (ly < kChebTS || ly >= kChebTS + kChebT || gy >= nx) continue;
+            const long long g = off + (long long)gy * nx + gx;
+            if (out_prev) out_prev[g] = pa[ly * R + cx];
+            out_cur[g] = pc[ly * R + cx];
+        }
     }
 }
 
@@ -540,7 +720,16 @@ void launch_kkt(cudaStream_t s, const ProbDev& P, const double* ty, const double
     const bool resid = part != nullptr;
     const long long N = P.ny;
     const unsigned grid = resid ? kRedBlocks : blocks_for(N);
-    if (P.heat) {
+    if (P.heat && g_kkt_tiled.load(std::memory_order_relaxed) && !P.M.coef && !P.Mtl.coef &&
+        !P.M.diag && !P.Mtl.diag) {
+        const long long nt = (long long)((P.nx + kKX - 1) / kKX) * ((P.nx + kKY - 1) / kKY) * P.nt;
+        const unsigned g = resid ? kRedBlocks : (unsigned)nt;
+        note_launch();
+        if (has_ty && resid) k_kkt_heat_tiled<true, true><<<g, 256, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else if (has_ty) k_kkt_heat_tiled<true, false><<<g, 256, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else if (resid) k_kkt_heat_tiled<false, true><<<g, 256, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        else k_kkt_heat_tiled<false, false><<<g, 256, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+    } else if (P.heat) {
         if (has_ty && resid) { note_launch(); k_kkt_heat<true, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
         else if (has_ty) { note_launch(); k_kkt_heat<true, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
         else if (resid) { note_launch(); k_kkt_heat<false, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
@@ -603,7 +792,7 @@ void launch_chebyshev(cudaStream_t s, const ProbDev& P, const double* b, const d
                 wk = (st == 2) ? 1.0 / (1.0 - 0.5 * rho * rho) : 1.0 / (1.0 - 0.25 * rho * rho * wk);
                 S.wk[i] = wk;
             }
-            constexpr size_t smem = 4 * (size_t)kChebR * kChebR * sizeof(double);
+            constexpr size_t smem = 2 * (size_t)(kChebR + 2) * kChebR * sizeof(double);
             static const bool attr = cudaFuncSetAttribute(k_cheb_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                           (int)smem) == cudaSuccess;
             (void)attr;
