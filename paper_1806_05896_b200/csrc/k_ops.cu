@@ -274,8 +274,11 @@ __global__ void __launch_bounds__(kT) k_kkt_heat(ProbDev P, const double* __rest
 // share y_k / p_k tiles run together and the re-read hits L2. RESID: the
 // fixed grid of kRedBlocks CTAs walks the tiles in a fixed order
 // (deterministic partials of |b - A x|^2).
+// The RESID launch has 512 threads: two independent 256-thread halves, each
+// walking its own tiles with its own named barrier, so the fixed grid still
+// keeps four tile pipelines per SM in flight.
 template <bool HAS_TY, bool RESID>
-__global__ void __launch_bounds__(256) k_kkt_heat_tiled(ProbDev P, const double* __restrict__ ty,
+__global__ void __launch_bounds__(RESID ? 512 : 256) k_kkt_heat_tiled(ProbDev P, const double* __restrict__ ty,
                                                         const double* __restrict__ tw,
                                                         const double* __restrict__ tv,
                                                         const double* __restrict__ x,
@@ -284,8 +287,14 @@ __global__ void __launch_bounds__(256) k_kkt_heat_tiled(ProbDev P, const double*
                                                         double* __restrict__ part)
 {
     constexpr int T = kKV * kKH;
-    __shared__ double sf[5 * T]; // y_k, y_{k-1}, p_k, p_{k+1}, w_k - v_k
+    extern __shared__ double kkt_sm[];
+    const int half = RESID ? (threadIdx.x >> 8) : 0;
+    double* sf = kkt_sm + half * 5 * T; // y_k, y_{k-1}, p_k, p_{k+1}, w_k - v_k
     __shared__ double sh[32];
+    auto half_sync = [&]() {
+        if (RESID) asm volatile("bar.sync %0, 256;" ::"r"(1 + half) : "memory");
+        else __syncthreads();
+    };
     const int nx = P.nx, nt = P.nt;
     const long long ns = P.ns, N = P.ny;
     const double* y = x;
@@ -294,15 +303,16 @@ __global__ void __launch_bounds__(256) k_kkt_heat_tiled(ProbDev P, const double*
     const double* p = x + 3 * N;
     const int tilesx = (nx + kKX - 1) / kKX, tilesy = (nx + kKY - 1) / kKY;
     const long long ntiles = (long long)tilesx * tilesy * nt;
-    const int tx = threadIdx.x & 31, tyy = threadIdx.x >> 5; // 8 warps
+    const int tx = threadIdx.x & 31, tyy = (threadIdx.x >> 5) & 7; // 8 warps per tile
     double acc = 0.0;
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long long tstep = RESID ? 2LL * gridDim.x : gridDim.x;
+    for (long long t = RESID ? 2LL * blockIdx.x + half : blockIdx.x; t < ntiles; t += tstep) {
         const int k = (int)(t % nt);
         const int ts = (int)(t / nt);
         const int x0 = (ts % tilesx) * kKX, y0 = (ts / tilesx) * kKY;
         const long long off = (long long)k * ns;
         const bool hm = k > 0, hp = k + 1 < nt;
-        __syncthreads(); // the previous tile's readers are done
+        half_sync(); // the previous tile's readers are done
         for (int r = tyy; r < kKV; r += 8) {
             const int gy = y0 + r - 1;
             const bool rok = gy >= 0 && gy < nx;
@@ -322,7 +332,7 @@ __global__ void __launch_bounds__(256) k_kkt_heat_tiled(ProbDev P, const double*
                 }
             }
         }
-        __syncthreads();
+        half_sync();
         const int gx = x0 + tx;
         const int ly = 2 * tyy; // rows ly, ly + 1 of the tile
         if (gx < nx && y0 + ly < nx) {
@@ -724,11 +734,18 @@ void launch_kkt(cudaStream_t s, const ProbDev& P, const double* ty, const double
         !P.M.diag && !P.Mtl.diag) {
         const long long nt = (long long)((P.nx + kKX - 1) / kKX) * ((P.nx + kKY - 1) / kKY) * P.nt;
         const unsigned g = resid ? kRedBlocks : (unsigned)nt;
+        constexpr size_t sm1 = 5 * (size_t)kKV * kKH * sizeof(double);
+        static const bool attr = [] { // the two-tile RESID variants exceed the 48 KB default
+            cudaFuncSetAttribute(k_kkt_heat_tiled<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sm1));
+            cudaFuncSetAttribute(k_kkt_heat_tiled<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sm1));
+            return true;
+        }();
+        (void)attr;
         note_launch();
-        if (has_ty && resid) k_kkt_heat_tiled<true, true><<<g, 256, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else if (has_ty) k_kkt_heat_tiled<true, false><<<g, 256, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else if (resid) k_kkt_heat_tiled<false, true><<<g, 256, 0, s>>>(P, ty, tw, tv, x, out, b, part);
-        else k_kkt_heat_tiled<false, false><<<g, 256, 0, s>>>(P, ty, tw, tv, x, out, b, part);
+        if (has_ty && resid) k_kkt_heat_tiled<true, true><<<g, 512, 2 * sm1, s>>>(P, ty, tw, tv, x, out, b, part);
+        else if (has_ty) k_kkt_heat_tiled<true, false><<<g, 256, sm1, s>>>(P, ty, tw, tv, x, out, b, part);
+        else if (resid) k_kkt_heat_tiled<false, true><<<g, 512, 2 * sm1, s>>>(P, ty, tw, tv, x, out, b, part);
+        else k_kkt_heat_tiled<false, false><<<g, 256, sm1, s>>>(P, ty, tw, tv, x, out, b, part);
     } else if (P.heat) {
         if (has_ty && resid) { note_launch(); k_kkt_heat<true, true><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
         else if (has_ty) { note_launch(); k_kkt_heat<true, false><<<grid, kT, 0, s>>>(P, ty, tw, tv, x, out, b, part); }
