@@ -201,3 +201,75 @@ def test_persistent_mgs_bitwise_equal(oc, ctx, lib, cfg):
     if name == "C3":
         assert max(out[1][1]) > 8
     assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+
+
+@pytest.mark.parametrize("solver", ["minres-pd", "gmres-pt"])
+def test_chained_heat_substitution_equals_per_block_launches(oc, ctx, lib, solver):
+    """One chained cluster launch per substitution direction (right-hand side
+    r_k + M x_{k-1} formed from the previous solution in shared memory,
+    timedep.cpp:268-311) reproduces the per-block launches (k_rhs_plus_mass +
+    one cluster launch per time block) bit for bit, Krylov counts included."""
+    from paper_1806_05896_b200 import configs
+
+    nt = 5
+    c = dataclasses.replace(configs.C5, horizon=nt * configs.C5.tau)
+    out = {}
+    try:
+        for v in (0, 1):
+            _tune(lib, b"heat_chain", v)
+            qp = oc.QpProblem(oc.ControlProblem(pde="heat", alpha=c.alpha, beta=c.beta, y_d=c.y_d(),
+                                                u_a=c.u_a, u_b=c.u_b, tau=c.tau, horizon=c.horizon),
+                              oc.Grid(c.level), ctx)
+            l0 = oc.Context.launch_count()
+            r = oc.ipm_solve(qp, oc.IpmParams(sigma=c.sigma, solver=solver))
+            out[v] = (r.u, r.state.y, [i.lin_iters for i in r.stats.iterations],
+                      oc.Context.launch_count() - l0)
+    finally:
+        _tune(lib, b"heat_chain", 1)
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+    assert out[1][3] < out[0][3]  # the chained path really ran (fewer launches)
+
+
+def test_tiled_heat_kkt_apply_equals_per_node_kernel(oc, ctx, lib):
+    """The shared-memory heat KKT apply (k_kkt_heat_tiled) gives the bits of the
+    per-node kernel on random x and Theta, first, interior and last time blocks
+    included (their neighbour-block terms are skipped, not zeroed)."""
+    from paper_1806_05896_b200 import configs
+
+    level, nt = 6, 4
+    c = configs.C5
+    yd = configs.sine_modes_spacetime(level, nt, c.tau, 42)
+    qp = oc.QpProblem(oc.ControlProblem(pde="heat", alpha=c.alpha, beta=c.beta, y_d=yd, u_a=c.u_a,
+                                        u_b=c.u_b, tau=c.tau, horizon=nt * c.tau), oc.Grid(level), ctx)
+    rng = np.random.default_rng(3)
+    ny = qp.ny
+    x = rng.standard_normal(4 * ny)
+    th = oc.ThetaBlocks(theta_y=None, theta_w=rng.random(ny) + 0.1, theta_v=rng.random(ny) + 0.1)
+    out = {}
+    try:
+        for v in (0, 1):
+            _tune(lib, b"kkt_tiled", v)
+            out[v] = np.array(qp.kkt_apply(th, x))
+    finally:
+        _tune(lib, b"kkt_tiled", 1)
+    assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("lean", [0, 2])
+def test_lean_variable_sweeps_bitwise_equal(oc, ctx, lib, lean):
+    """Variable-coefficient tiled sweeps that read 1/a_ii (and b) in the colour
+    passes instead of staging them (sweep_lean) reproduce the default bits."""
+    ell = 9
+    L = oc.assemble9("convdiff", ell, eps=0.02)
+    L[4] += 1.0
+    b = np.random.default_rng(11).uniform(-1, 1, L.shape[1])
+    out = {}
+    try:
+        for v in (1, lean):
+            _tune(lib, b"sweep_lean", v)
+            mg = oc.MgHierarchy(L, ell, rediscretize=1, eps=0.02, ctx=ctx)
+            out[v] = mg.solve(b, 2, 5, 5)
+    finally:
+        _tune(lib, b"sweep_lean", 1)
+    assert np.array_equal(out[1], out[lean])
