@@ -341,7 +341,8 @@ def measured_traffic(kernel):
         except Exception:
             continue
         if d.get("kernel") == kernel:
-            best = {"bytes": d["dram_bytes_per_launch"], "source": os.path.relpath(f, ROOT)}
+            best = {"bytes": d["dram_bytes_per_launch"], "source": os.path.relpath(f, ROOT),
+                    "blocks_per_launch": d.get("blocks_per_launch", 1)}
     return best
 
 
@@ -528,6 +529,10 @@ def run_ours_c5(args, torch, dist, rank, world, local):
     kkt_b, prec_b = bytes_model.apply_bytes(kind, c.level, ny, pde="heat")
     kkt_ms, prec_ms = qps[0].time_applies(kind, 3)
     apply_gbs = (kkt_b + prec_b) / ((kkt_ms + prec_ms) / 1e3) / 1e9
+    # all replicas together: every KKT + P_D apply of the timed steps (one of each per Krylov
+    # iteration plus the P_D apply that starts each Newton solve) over the steps' device time
+    n_applies = sum(r.total_lin + r.stats.nli for res in results for r in res)
+    agg_gbs = n_applies * (kkt_b + prec_b) / (max_ms / 1e3) / 1e9  # this rank's GPU
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -592,7 +597,13 @@ def run_ours_c5(args, torch, dist, rank, world, local):
         "kkt_precond_apply": {"gbs": apply_gbs, "kkt_ms": kkt_ms, "prec_ms": prec_ms,
                               "bytes": kkt_b + prec_b, "frac_of_peak": apply_gbs / peak,
                               "how": "oc_time_applies on replica 0 alone after its last solve "
-                                     "(final Theta), CUDA events; SURVEY 8d byte model"},
+                                     "(final Theta), CUDA events; SURVEY 8d byte model",
+                              "in_flight": {"gbs": agg_gbs, "frac_of_peak": agg_gbs / peak,
+                                            "applies": n_applies, "solves_in_flight": R,
+                                            "how": "algorithmic bytes of every KKT + P_D apply of "
+                                                   "the timed steps (all solves in flight on this "
+                                                   "GPU) / the steps' device time, setup and "
+                                                   "Krylov vector work included in the time"}},
     }
 
 
