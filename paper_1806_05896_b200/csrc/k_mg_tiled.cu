@@ -201,13 +201,14 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     // node sit at pass-uniform offsets from k in the other planes.
     constexpr int CXN = S::CXN, KC = S::KC, KT = (KC + 255) / 256;
     static_assert(RX % 2 == 0 && RY % 2 == 0, "even regions keep colour parity");
-    int kx0[KT], ky0[KT];
+    int kx0[KT], ky0[KT], ks0[KT];
 #pragma unroll
     for (int m = 0; m < KT; ++m) {
         const int k = threadIdx.x + 256 * m;
         const int ky = k / CXN, kx = k - ky * CXN;
         kx0[m] = k < KC ? ox + 2 * kx : -(1 << 30); // out-of-range marker
         ky0[m] = oy + 2 * ky;
+        ks0[m] = ky0[m] * nx + (ox >> 1) + kx; // colour-split node index less the pass offset
     }
     long long cpo[9]; // coefficient plane offsets d * n (variable operators)
 #pragma unroll
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         const int lox = max(tx0 - g, 0), hix = min(tx0 + TX + g, nx);
         const int loy = max(ty0 - g, 0), hiy = min(ty0 + TY + g, nx);
         const int lc = c * PS;
+        const int so = cy * nx + (cx ? ((nx + 1) >> 1) : 0); // colour-split index offset of this pass
         int off[9]; // neighbour d of a colour-c node k: xs[off[d] + k]
 #pragma unroll
         for (int d = 0; d < 9; ++d) {
@@ -239,15 +241,31 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 const double* cp = VAR ? A.coef + ((long long)gy * nx + gx) : nullptr;
                 const long long gi = (long long)gy * nx + gx;
                 double s = LEAN == 2 ? __ldg(b + gi) : bs[l];
+                if (VAR && !S::CS && A.csplit) {
+                    // the node's record: 8 off-diagonals in four 16-byte loads
+                    const int si = ks0[m] + so;
+                    const double2* rec = reinterpret_cast<const double2*>(A.csplit) + (long long)si * 4;
+                    const double2 a01 = __ldg(rec), a23 = __ldg(rec + 1), a45 = __ldg(rec + 2),
+                                  a67 = __ldg(rec + 3);
+                    const double ivl = LEAN >= 1 ? __ldg(A.isplit + si) : iv[l];
+                    s -= a01.x * xs[off[0] + k];
+                    s -= a01.y * xs[off[1] + k];
+                    s -= a23.x * xs[off[2] + k];
+                    s -= a23.y * xs[off[3] + k];
+                    s -= a45.x * xs[off[5] + k];
+                    s -= a45.y * xs[off[6] + k];
+                    s -= a67.x * xs[off[7] + k];
+                    s -= a67.y * xs[off[8] + k];
+                    xs[l] = s * ivl;
+                    continue;
+                }
                 const double ivl = LEAN >= 1 ? __ldg(inv + gi) : iv[l];
 #pragma unroll
                 for (int d = 0; d < 9; ++d) {
                     if (d == 4) continue;
                     double a;
                     if (S::CS) a = cs[(d < 4 ? d : d - 1) * RP + l];
-                    else if (VAR) a = A.csplit ? __ldg(A.csplit + (long long)(d < 4 ? d : d - 1) * n + gy * nx +
-                                                       ((gx & 1) ? ((nx + 1) >> 1) + (gx >> 1) : (gx >> 1)))
-                                               : __ldg(cp + cpo[d]);
+                    else if (VAR) a = __ldg(cp + cpo[d]);
                     else a = A.c[d];
                     s -= a * xs[off[d] + k];
                 }
@@ -426,17 +444,27 @@ __global__ void __launch_bounds__(256) k_resid_restrict(Op9 A, const double* __r
     }
 }
 
-// colour-split copy of the off-diagonal planes: row y holds its even-x nodes,
-// then its odd-x nodes, so one colour pass of the tiled sweep reads whole sectors
-__global__ void k_colour_split(int nx, const double* __restrict__ coef, double* __restrict__ out)
+// colour-split copy of a variable operator for the tiled sweep: row y holds its
+// even-x nodes, then its odd-x nodes, so one colour pass reads consecutive
+// node records: the 8 off-diagonals of a node next to each other (four 16-byte
+// loads from one address instead of eight strided planes), and 1/a_ii
+// (k_inv_diag's quotient) in the same node order
+__global__ void k_colour_split(int nx, const double* __restrict__ coef, const double* __restrict__ diag,
+                               double* __restrict__ out, double* __restrict__ iout)
 {
     const long long n = (long long)nx * nx;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int gy = (int)(i / nx), gx = (int)(i - (long long)gy * nx);
     const long long o = (long long)gy * nx + ((gx & 1) ? ((nx + 1) >> 1) + (gx >> 1) : (gx >> 1));
-    const int p = blockIdx.y, d = p < 4 ? p : p + 1;
-    out[p * n + o] = coef[d * n + i];
+    const int p = blockIdx.y;
+    if (p < 8) {
+        out[o * 8 + p] = coef[(p < 4 ? p : p + 1) * n + i];
+    } else {
+        double a = coef[4 * n + i];
+        if (diag) a += diag[i];
+        iout[o] = 1.0 / a;
+    }
 }
 
 __global__ void k_inv_diag(Op9 A, double* __restrict__ inv, long long fcs, long long fds,
@@ -540,11 +568,12 @@ std::atomic<int> g_colour_split{1};
 std::atomic<int> g_fuse_norm{1};
 std::atomic<int> g_fuse_restrict{1};
 
-void launch_colour_split(cudaStream_t s, int nx, const double* coef, double* out)
+void launch_colour_split(cudaStream_t s, int nx, const double* coef, const double* diag, double* out,
+                         double* iout)
 {
     const long long n = (long long)nx * nx;
     note_launch();
-    k_colour_split<<<dim3((unsigned)((n + 255) / 256), 8), 256, 0, s>>>(nx, coef, out);
+    k_colour_split<<<dim3((unsigned)((n + 255) / 256), 9), 256, 0, s>>>(nx, coef, diag, out, iout);
 }
 
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,
