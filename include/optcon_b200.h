@@ -218,14 +218,20 @@ int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
  * "colour_split" (1: variable levels >= 511^2 sweep from a colour-split
  * coefficient copy), "cheb_block" (1: 5 Chebyshev steps per launch),
  * "fuse_norm" (1: a V-cycle's last sweep launch runs the divergence check),
- * "kkt_tiled" (1: the steady KKT apply from shared-memory halo tiles),
+ * "kkt_tiled" (1: the steady and the heat KKT apply from shared-memory halo
+ * tiles), "heat_fork" (1: heat P_D's time-block substitution on the
+ * high-priority side stream), "heat_chain" (1: each direction of the heat
+ * time-block substitution as one chained cluster launch), "sweep_lean"
+ * (variable tiled sweeps: 1 = 1/a_ii, 2 = 1/a_ii and b read in the colour
+ * passes instead of staged; default 1),
  * "lex_bottom_top" (lexicographic mode: top level of the single-CTA bottom
  * solver, 3..6, default 4; higher levels sweep as multi-CTA wavefronts),
  * "fuse_restrict" (1: a level's last pre-smoothing launch restricts its
  * residual), "mgs_persistent" (GMRES columns with j+1 >= value run their
  * modified Gram-Schmidt in one cooperative launch; default 8, 0 never).
  * Only launch shapes or layouts differ; results agree to rounding, and bit
- * for bit for the last six. */
+ * for bit for every knob but the tile/fuse shapes and the cluster bottoms
+ * ("kkt_tiled" regroups only the residual-norm partial sums). */
 int oc_set_tuning(const char* name, int value);
 /* Test hook: the lexicographic update's quotient (RN(1/d) product plus one
  * Markstein correction) against div.rn.f64 on n operand pairs (host or device

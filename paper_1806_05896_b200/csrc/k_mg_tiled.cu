@@ -3,12 +3,18 @@
 // k_sweep<TX,TY,NS,VAR>: NS symmetric-colour Gauss-Seidel sweeps (4 colour
 // passes each, multigrid.cpp:44-66 restated as the 4-colour variant) over one
 // TX x TY output tile per CTA. The tile plus a halo of 4*NS nodes is staged in
-// shared memory with asynchronous copies (cp.async, all in flight at once):
-// x, b, the reciprocal diagonal and, for variable operators, the 8
-// off-diagonal coefficient planes. Pass q then updates the colour nodes of the
-// tile grown by 4*NS-1-q entirely from shared memory, so after all passes the
-// tile is exact without inter-CTA synchronisation (redundant halo work).
-// Threads form a 32x8 grid mapped onto the colour sub-lattice (no division).
+// shared memory with asynchronous copies (cp.async, all in flight at once) in
+// a colour-planar layout (one plane per colour, so a colour pass reads every
+// operand at unit stride: no bank conflicts): x, b, the reciprocal diagonal
+// and, for small variable tiles, the 8 off-diagonal coefficient planes. Pass q
+// then updates the colour nodes of the tile grown by 4*NS-1-q entirely from
+// shared memory, so after all passes the tile is exact without inter-CTA
+// synchronisation (redundant halo work). Large variable levels read their
+// coefficients in the passes from a colour-split copy of per-node records
+// (8 off-diagonals = four 16-byte loads from one address; Op9::csplit) with
+// 1/a_ii in the same order, which leaves room for five CTAs per SM.
+// Threads own fixed positions k = t + 256 m of the colour sub-lattice, which
+// are also the shared-memory indices inside a colour plane.
 //
 // k_resid_restrict<VAR>: r = b - A x on the fine nodes of a coarse tile (x and
 // coefficients staged the same way), then rc = R r with R = P^T
