@@ -690,7 +690,22 @@ __global__ void __launch_bounds__(kCT, 1)
     const double* __restrict__ bg = bg0 + ob * ch.ns;
     double* __restrict__ xg = xg0 + ob * ch.ns;
     const double* diag8 = (S8 && a.ops[0].diag) ? a.ops[0].diag + ob * ch.ns : nullptr;
-    // ---- load. Level 8: b and 1/a_ii of the thread's 16 nodes in registers.
+    // ---- load. First the asynchronous copies (they complete while the register
+    // rows below are loaded): levels <= 4 are CTAs 1..15 holding 15 rows each of
+    // the dense level-4 V-cycle operator (k_coarse_op) where CTA 0 keeps level 5
+    // (the region's last readers finished before the previous element's closing
+    // cluster barrier)
+    double* cops = c0base;
+    if (w > 0) {
+        const double* src = a.cop + ob * kCopN * kCopN + (size_t)kCopRows * kCopN * (w - 1);
+        for (int i = threadIdx.x; i < kCopRows * kCopN; i += blockDim.x) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(cops + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src + i) : "memory");
+        }
+    } else {
+        C0Cycle<NC>::load_top(c0base, a, K0 + (Ly::S1 ? 2 : 1), ob * 9 * NC * NC);
+    }
+    // Level 8: b and 1/a_ii of the thread's 16 nodes in registers.
     double rb8[S8 ? G8::NPT : 1][4] = {}, ri8[S8 ? G8::NPT : 1][4] = {};
     if constexpr (S8) {
         const Op9& A = a.ops[0];
@@ -760,20 +775,7 @@ __global__ void __launch_bounds__(kCT, 1)
             }
         }
     }
-    // levels <= 4: CTAs 1..15 hold 15 rows each of the dense level-4 V-cycle
-    // operator (k_coarse_op) where CTA 0 keeps level 5
-    double* cops = c0base;
-    if (w > 0) {
-        const double* src = a.cop + ob * kCopN * kCopN + (size_t)kCopRows * kCopN * (w - 1);
-        for (int i = threadIdx.x; i < kCopRows * kCopN; i += blockDim.x) {
-            const unsigned dst = (unsigned)__cvta_generic_to_shared(cops + i);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src + i) : "memory");
-        }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-    } else {
-        C0Cycle<NC>::load_top(c0base, a, K0 + (Ly::S1 ? 2 : 1), ob * 9 * NC * NC);
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory"); // level 5 / dense rows
     cl.sync();
     probe(w, 1);
 
