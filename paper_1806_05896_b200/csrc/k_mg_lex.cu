@@ -31,6 +31,21 @@
 // (it needs the mailbox chunk ahead) and reads the rows of the band below
 // (its row 32) at most 4 chunks ahead.
 //
+// Pipelined batches: the 5 sweeps of a smoothing phase are 5 launches on 5
+// streams (Hierarchy::lex_sweeps). Sweep q+1 reads what sweep q wrote, so its
+// staging warps wait, before loading chunk c, until sweep q's same band has
+// written chunk c back and the band below chunk c-4 (the columns of its first
+// row that chunk c stages as row 32); a band publishes its written-back chunk
+// count after each period's barrier (fence + relaxed store, acquire loads on
+// the other side). Each sweep has its own mailbox set. Sweep q+1 then trails
+// sweep q by a few chunks per band instead of a whole sweep (level 10:
+// 5 sweeps in ~1.2 sweep times), and nothing it overwrites is still needed by
+// sweep q: band w of sweep q+1 writes chunk c only after sweep q's band w wrote
+// it, which is after sweep q's band w-1 read it as its row 32. Every wait
+// points to an earlier launch or an earlier block of the same launch, so the
+// earliest unfinished block can always run (no deadlock when the 160 blocks of
+// a level-10 batch exceed the 148 SMs).
+//
 // Backward sweeps (rows and columns descending) run the same code in
 // mirrored coordinates: logical (x, r) is physical (nx-1-x, nx-1-r) and
 // stencil entry d becomes 8-d; the physical ascending column order is then
@@ -102,7 +117,20 @@ struct LexArgs {
     double* mbox;
     int* flags;
     int start_col; // column of the band above that starts a band (hand-over lag)
+    // Pipelined sweeps (several sweeps of one level in flight, one launch each on
+    // its own stream): prog_prev[band] = chunks the PREVIOUS sweep's band has
+    // written back (nullptr: nothing to wait for), prog_out[band] = this sweep's.
+    const int* prog_prev;
+    int* prog_out;
 };
+
+__device__ __forceinline__ int ld_acquire_int(const int* p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+constexpr int kLexDone = 1 << 28; // progress value of a finished band
 
 template <bool VAR, bool FWD>
 __global__ void __launch_bounds__(LexSlot<VAR>::kThreads, 1) k_gs_lex(LexArgs a)
@@ -149,9 +177,38 @@ __global__ void __launch_bounds__(LexSlot<VAR>::kThreads, 1) k_gs_lex(LexArgs a)
         constexpr int NP = 16 / NSW; // row pairs per staging warp
         double reg[2][NP][NA + 1];
         double reg32[2] = {0.0, 0.0};
+        int pstall = 0;
+        // previous sweep of a pipelined batch: chunk c of this band reads its own
+        // rows after that sweep (its band w wrote chunk c back) and, as row 32,
+        // columns [16c - 64, 16c - 48) of band w+1's first row (its chunk c - 4)
+        auto wait_prev = [&](int c) {
+            if (!a.prog_prev) return;
+            if (j == 0) {
+                const int need0 = min(c + 1, nchunks), need1 = min(c - 3, nchunks);
+                while (ld_acquire_int(a.prog_prev + w) < need0)
+                    if (++pstall > kLexSpinLimit) {
+                        atomicOr(a.flags, kErrLexStall);
+                        break;
+                    }
+                if (produces && need1 > 0)
+                    while (ld_acquire_int(a.prog_prev + w + 1) < need1)
+                        if (++pstall > kLexSpinLimit) {
+                            atomicOr(a.flags, kErrLexStall);
+                            break;
+                        }
+            }
+            __syncwarp();
+        };
+        auto publish = [&](int done) { // after a barrier that follows the write-backs
+            if (a.prog_out && sw == 0 && j == 0) {
+                __threadfence();
+                asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(a.prog_out + w), "r"(done) : "memory");
+            }
+        };
         auto load = [&](int c, auto bufc) {
             constexpr int B = decltype(bufc)::value;
             const int ic = i00 + c * dc;
+            wait_prev(c);
 #pragma unroll
             for (int t = 0; t < NP; ++t) {
                 const int p = sw + t * NSW;
@@ -264,6 +321,7 @@ __global__ void __launch_bounds__(LexSlot<VAR>::kThreads, 1) k_gs_lex(LexArgs a)
             load(c + 4, bufc);
             mailbox(c + 1);
             __syncthreads();
+            publish(c); // chunks 0 .. c-1 are in global memory
         };
 #pragma unroll 1
         for (int c = 0; c < nchunks; c += 2) {
@@ -271,6 +329,10 @@ __global__ void __launch_bounds__(LexSlot<VAR>::kThreads, 1) k_gs_lex(LexArgs a)
             if (c + 1 < nchunks) period(c + 1, B1{});
         }
         writeback(nchunks - 1);
+        if (a.prog_out) {
+            asm volatile("bar.sync 1, %0;" ::"r"(NSW * 32) : "memory"); // the staging warps
+            publish(kLexDone);
+        }
         // every value of the band above has been consumed (its producer is
         // done): restore the sentinels in one coalesced pass
         if (consumer)
@@ -388,11 +450,15 @@ void go(cudaStream_t s, const LexArgs& a)
 
 std::atomic<int> g_lex_bottom_top{4};
 std::atomic<int> g_lex_start{17};
+std::atomic<int> g_lex_pipeline{1}; // 1: the sweeps of a smoothing phase run as a pipelined batch
 
 void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* inv,
-                   const double* dfull, double* x, bool forward, double* mbox, int* flags)
+                   const double* dfull, double* x, bool forward, double* mbox, int* flags,
+                   const int* prog_prev, int* prog_out)
 {
     LexArgs a{};
+    a.prog_prev = prog_prev;
+    a.prog_out = prog_out;
     a.nx = A.nx;
     a.b = b;
     a.inv = inv;

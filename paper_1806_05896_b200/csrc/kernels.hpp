@@ -96,7 +96,12 @@ void launch_bottom(cudaStream_t s, const BottomArgs& a, const double* b, double*
 // mbox = ceil(nx/32) * nx doubles holding kLexSentinel (restored on return).
 // dfull = a_ii (the CSR diagonal value: centre coefficient + added diagonal).
 void launch_gs_lex(cudaStream_t s, const Op9& A, const double* b, const double* inv,
-                   const double* dfull, double* x, bool forward, double* mbox, int* flags);
+                   const double* dfull, double* x, bool forward, double* mbox, int* flags,
+                   const int* prog_prev = nullptr, int* prog_out = nullptr);
+// Pipelined batch of lexicographic sweeps (k_mg_lex.cu, LexArgs::prog_*): up to
+// kLexPipe sweeps of one level in flight, each launch with its own mailbox set.
+constexpr int kLexPipe = 5;
+extern std::atomic<int> g_lex_pipeline;
 // test hook: mismatches of the lexicographic update's quotient vs div.rn.f64
 void launch_lex_div_check(cudaStream_t s, const double* num, const double* den, long long n,
                           unsigned long long* bad);

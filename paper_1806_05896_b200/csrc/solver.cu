@@ -130,6 +130,11 @@ Ctx::Ctx(int dev) : device(dev)
     cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
     cuda_check(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi), "cudaStreamCreate");
     cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&lex_fork, cudaEventDisableTiming), "cudaEventCreate");
+    for (int q = 0; q < kLexPipe - 1; ++q) {
+        cuda_check(cudaStreamCreateWithFlags(&lexs[q], cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaEventCreateWithFlags(&lex_ev[q], cudaEventDisableTiming), "cudaEventCreate");
+    }
     cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaEventCreate(&ev0), "cudaEventCreate");
     cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
@@ -154,6 +159,14 @@ Ctx::~Ctx()
         cudaStreamSynchronize(side);
         cudaStreamDestroy(side);
     }
+    for (int q = 0; q < kLexPipe - 1; ++q) {
+        if (lexs[q]) {
+            cudaStreamSynchronize(lexs[q]);
+            cudaStreamDestroy(lexs[q]);
+        }
+        if (lex_ev[q]) cudaEventDestroy(lex_ev[q]);
+    }
+    if (lex_fork) cudaEventDestroy(lex_fork);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream) cudaStreamDestroy(stream);
@@ -230,7 +243,8 @@ void Hierarchy::allocate(int level, int batch, int smoother)
     }
     if (lex_) {
         const int nx0 = nx_[0];
-        mbox_.resize((size_t)((nx0 + 31) / 32) * nx0);
+        mbox_.resize((size_t)kLexPipe * ((nx0 + 31) / 32) * nx0);
+        prog_.resize((size_t)kLexPipe * ((nx0 + 31) / 32 + 1));
     } else {
         mbox_.release();
     }
@@ -389,6 +403,40 @@ BottomArgs Hierarchy::bottom_args(int kfrom, int bt) const
     return a;
 }
 
+void Hierarchy::lex_sweeps(Ctx& c, const Op9& A, const double* b, int k, int bt, double* x,
+                           bool forward, int count, int* flags)
+{
+    const double* inv = inv_at(k, bt);
+    const double* dfull = dfull_at(k, bt);
+    const int nb0 = (nx_[0] + 31) / 32;
+    const size_t mstride = (size_t)nb0 * nx_[0]; // one mailbox set
+    const int pstride = nb0 + 1;
+    if (!g_lex_pipeline.load() || count < 2) {
+        for (int s = 0; s < count; ++s)
+            launch_gs_lex(c.stream, A, b, inv, dfull, x, forward, mbox_.get(), flags);
+        return;
+    }
+    // Sweep q+1 of a batch trails sweep q by a few chunks per band instead of
+    // a whole sweep: every sweep is its own launch on its own stream (fork /
+    // join by events, capturable), with its own mailbox set; the kernels pace
+    // each other through per-band progress counters (k_mg_lex.cu).
+    for (int done = 0; done < count; done += kLexPipe) {
+        const int m = std::min(kLexPipe, count - done);
+        cuda_check(cudaMemsetAsync(prog_.get(), 0, sizeof(int) * (size_t)m * pstride, c.stream), "memset");
+        cuda_check(cudaEventRecord(c.lex_fork, c.stream), "cudaEventRecord");
+        for (int q = 0; q < m; ++q) {
+            cudaStream_t sq = q == 0 ? c.stream : c.lexs[q - 1];
+            if (q > 0) cuda_check(cudaStreamWaitEvent(sq, c.lex_fork, 0), "cudaStreamWaitEvent");
+            launch_gs_lex(sq, A, b, inv, dfull, x, forward, mbox_.get() + q * mstride, flags,
+                          q > 0 ? prog_.get() + (size_t)(q - 1) * pstride : nullptr,
+                          q + 1 < m ? prog_.get() + (size_t)q * pstride : nullptr);
+            if (q > 0) cuda_check(cudaEventRecord(c.lex_ev[q - 1], sq), "cudaEventRecord");
+        }
+        for (int q = 1; q < m; ++q)
+            cuda_check(cudaStreamWaitEvent(c.stream, c.lex_ev[q - 1], 0), "cudaStreamWaitEvent");
+    }
+}
+
 void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_in,
                        const MgParams& p, int bt, int* flags, bool* fused_norm)
 {
@@ -405,13 +453,11 @@ void Hierarchy::vcycle(Ctx& c, int k, const double* b, double* xout, bool zero_i
     if (lex_) {
         // reference cycle (multigrid.cpp:111-132) with in-place lexicographic sweeps
         if (zero_in) launch_fill(c.stream, xout, 0.0, level_n(k));
-        for (int s = 0; s < p.pre; ++s)
-            launch_gs_lex(c.stream, A, b, inv_at(k, bt), dfull_at(k, bt), xout, true, mbox_.get(), flags);
+        lex_sweeps(c, A, b, k, bt, xout, true, p.pre, flags);
         launch_resid_restrict_tiled(c.stream, A, b, xout, b_[k + 1].get(), xa_[k + 1].get());
         vcycle(c, k + 1, b_[k + 1].get(), xa_[k + 1].get(), true, p, bt, flags);
         launch_prolong_add(c.stream, nx_[k], xa_[k + 1].get(), xout);
-        for (int s = 0; s < p.post; ++s)
-            launch_gs_lex(c.stream, A, b, inv_at(k, bt), dfull_at(k, bt), xout, false, mbox_.get(), flags);
+        lex_sweeps(c, A, b, k, bt, xout, false, p.post, flags);
         return;
     }
     double* Abuf = xout;
@@ -1049,7 +1095,12 @@ void Problem::precond_apply(int kind, const double* r, double* out)
         const char* e = getenv("OC_GRAPHS");
         return e && e[0] == '0';
     }();
-    if (env_off || !graphs_enabled_ || ctx.prof.on) {
+    // Lexicographic mode runs directly: its applies are tens of milliseconds of
+    // wavefront kernels (launch overhead does not matter), GMRES uses every
+    // (r, out) pair only once per Newton step, and instantiating the
+    // multi-stream graphs of the pipelined sweep batches costs more than their
+    // replays save (C3 at 257^2: 26.1 s with graphs, 12.7 s without).
+    if (env_off || !graphs_enabled_ || ctx.prof.on || smoother_ == OC_SMOOTHER_LEX) {
         precond_apply_direct(kind, r, out);
         return;
     }

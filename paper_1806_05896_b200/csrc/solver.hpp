@@ -103,6 +103,8 @@ struct Ctx {
     // apply runs on it, forked from / joined to `stream` by two events, while
     // the Chebyshev and 2x2 blocks run on `stream`
     cudaStream_t side = nullptr;
+    cudaStream_t lexs[kLexPipe - 1] = {}; // sweeps 2.. of a pipelined lexicographic batch
+    cudaEvent_t lex_fork = nullptr, lex_ev[kLexPipe - 1] = {};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t user_ev[8] = {};
@@ -195,7 +197,11 @@ private:
     int level_ = 0, K_ = 0, kb_ = 0, batch_ = 1, smoother_ = OC_SMOOTHER_COLOR4;
     bool lex_ = false;     // lexicographic smoother: in-place wavefront sweeps, single-CTA bottom
     long long gen_ = 0;
-    DVec mbox_;            // wavefront hand-off mailbox (lex), ceil(nx/32) * nx sentinels
+    DVec mbox_;            // wavefront hand-off mailboxes (lex): kLexPipe sets of ceil(nx/32) * nx sentinels
+    DevArray<int> prog_;   // per-band progress counters of a pipelined batch (kLexPipe x (bands + 1))
+    // `count` lexicographic sweeps of level k (pipelined when enabled)
+    void lex_sweeps(Ctx& c, const Op9& A, const double* b, int k, int bt, double* x, bool forward,
+                    int count, int* flags);
     bool cluster_ = false;  // bottom levels run in the 16-CTA cluster kernel
     std::vector<int> nx_;
     Op9 fine_{};

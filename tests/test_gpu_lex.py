@@ -104,6 +104,34 @@ def test_lex_sweeps_repeat_bitwise(oc, ctx):
         assert np.array_equal(mg.smooth(b, x0, False), first[1])
 
 
+@pytest.mark.parametrize("ell,kind,sweeps", [(7, "poisson", 5), (8, "convdiff", 5), (9, "convdiff", 7),
+                                             (9, "poisson", 2), (10, "convdiff", 5)])
+def test_pipelined_lex_batches_equal_sequential_sweeps(oc, ctx, ell, kind, sweeps):
+    """The sweeps of a smoothing phase launched as a pipelined batch (one launch
+    per sweep on its own stream, paced by per-band progress counters, one
+    mailbox set each; more than five sweeps split into batches) give the bits of
+    the one-after-the-other launches, forward and backward, repeatedly."""
+    from paper_1806_05896_b200 import _lib
+
+    lib = _lib.load()
+    A = oc.assemble9(kind, ell, eps=0.02) if kind == "convdiff" else oc.assemble9(kind, ell)
+    A[4] += 1.0
+    b = np.random.default_rng(13).uniform(-1, 1, A.shape[1])
+    out = {}
+    try:
+        for v in (0, 1, 1):
+            _lib.check(lib.oc_set_tuning(b"lex_pipeline", v))
+            mg = oc.MgHierarchy(A, ell, ctx=ctx, smoother="lex")
+            x = mg.solve(b, 2, sweeps, sweeps)
+            if v in out:
+                assert np.array_equal(out[v], x)  # rerun: mailboxes and counters were left clean
+            out[v] = x
+            mg.close()
+    finally:
+        _lib.check(lib.oc_set_tuning(b"lex_pipeline", 1))
+    assert np.array_equal(out[0], out[1])
+
+
 @pytest.mark.parametrize("ell", [4, 6, 7, 9])
 def test_lex_vcycle_matches_reference_library(oc, ctx, refmod, ell):
     A = operator(oc, "poisson+diag", ell, 7 + ell)
