@@ -211,7 +211,7 @@ int oc_debug_cluster_probes(int enable, unsigned long long* out64);
    cluster bottom applies (row-major, batch element 0) */
 int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
 /* Tuning knobs (process-wide): "sweep_tile" (-1 auto, 0: 64x32, 1: 32x32,
- * 2: 32x16, 3: 16x16 output tiles), "sweep_fuse" (1..5 smoothing sweeps per
+ * 2: 32x16, 3: 16x16, 4: 32x24 output tiles), "sweep_fuse" (1..5 smoothing sweeps per
  * launch, default 2), "cluster_bottom" (1: levels <= 7 in the 16-CTA cluster
  * kernel, 0: single-CTA bottom), "cluster_top8" (1: constant-stencil level-8
  * hierarchies, e.g. heat time blocks, solved whole in the cluster kernel),

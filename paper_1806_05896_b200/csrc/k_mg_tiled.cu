@@ -559,6 +559,13 @@ void sweep_tile(int id, cudaStream_t s, const Op9& A, const double* b, const dou
         [[fallthrough]];
     case 1: sweep_pick_var<32, 32, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro); break;
     case 2: sweep_pick_var<32, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro); break;
+    case 4:
+        if constexpr (NS <= 2) {
+            sweep_pick_var<32, 24, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
+            break;
+        }
+        sweep_pick_var<32, 32, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
+        break;
     default: sweep_pick_var<16, 16, NS>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro); break;
     }
 }
@@ -601,14 +608,16 @@ bool launch_sweep_tiled(cudaStream_t s, const Op9& A, const double* b, const dou
         // With several solves in flight (one context each) the sweeps compete
         // for bandwidth: prefer the larger tiles (less halo re-read).
         const bool shared = active_contexts() > 1;
-        if (A.nx >= 1000) id = 1;
+        // variable 1023^2 levels: 32x24 tiles = 1376 CTAs = 1.86 waves of the 740
+        // resident CTAs (32x32: 1024 = 1.38 waves, a second round 38% full)
+        if (A.nx >= 1000) id = A.coef ? 4 : 1;
         else if (A.nx >= 500) id = shared ? (A.coef ? 1 : 0) : 2;
         else id = (shared && A.coef) ? 1 : 3;
     }
     if (id == 0 && (A.coef || ns > 2)) id = 1; // 64x32 tiles: constant stencils, <= 2 sweeps
     // fuse the divergence check when asked for, the launch sweeps <= 2 times and
     // its grid fits the partials buffer (kNormBlocks)
-    const int T = id == 0 ? 64 : 32, TYy = id == 0 ? 32 : (id == 1 ? 32 : (id == 2 ? 16 : 16));
+    const int T = id == 0 ? 64 : 32, TYy = id == 0 ? 32 : (id == 1 ? 32 : (id == 4 ? 24 : 16));
     const int TXx = id == 3 ? 16 : T;
     const long long nb = (long long)((A.nx + TXx - 1) / TXx) * ((A.nx + TYy - 1) / TYy);
     NormCheck nc{part, counter, state, flags};
