@@ -224,7 +224,9 @@ int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
  * time-block substitution as one chained cluster launch), "sweep_lean"
  * (variable tiled sweeps: 1 = 1/a_ii, 2 = 1/a_ii and b read in the colour
  * passes instead of staged; default 1),
- * "lex_pipeline" (1: the lexicographic sweeps of a smoothing phase run as a
+ * "gmres_lazy_residual" (1: GMRES rebuilds x and forms the true residual only
+ * once the residual norm it carries is within 1e3 of the tolerance, and at
+ * every exit), "lex_pipeline" (1: the lexicographic sweeps of a smoothing phase run as a
  * pipelined batch of concurrent launches), "lex_bottom_top" (lexicographic
  * mode: top level of the single-CTA bottom
  * solver, 3..6, default 4; higher levels sweep as multi-CTA wavefronts),

@@ -467,6 +467,7 @@ int oc_set_tuning(const char* name, int value)
         else if (k == "heat_fork") ocb::g_heat_fork = value;
         else if (k == "heat_chain") ocb::g_heat_chain = value;
         else if (k == "lex_pipeline") ocb::g_lex_pipeline = value;
+        else if (k == "gmres_lazy_residual") ocb::g_gmres_lazy_residual = value;
         else if (k == "lex_start") ocb::g_lex_start = value < 17 ? 17 : value;
         else if (k == "lex_bottom_top") ocb::g_lex_bottom_top = value < 3 ? 3 : (value > 6 ? 6 : value);
         else throw ocb::InvalidArgument("oc_set_tuning: unknown knob " + k);
@@ -495,6 +496,7 @@ int oc_get_tuning(const char* name, int* value)
         else if (k == "heat_fork") *value = ocb::g_heat_fork;
         else if (k == "heat_chain") *value = ocb::g_heat_chain;
         else if (k == "lex_pipeline") *value = ocb::g_lex_pipeline;
+        else if (k == "gmres_lazy_residual") *value = ocb::g_gmres_lazy_residual;
         else if (k == "lex_start") *value = ocb::g_lex_start;
         else if (k == "lex_bottom_top") *value = ocb::g_lex_bottom_top;
         else throw ocb::InvalidArgument("oc_get_tuning: unknown knob " + k);

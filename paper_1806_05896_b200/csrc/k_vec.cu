@@ -659,6 +659,25 @@ void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, 
     else k_gmres_givens<<<1, kGivT, 0, s>>>(part, G, j);
 }
 
+// |g_{j+1}| (the least-squares residual norm GMRES carries, = ||b - A x_j|| in exact
+// arithmetic) with the error flags and stop code next to it, for the iterations
+// whose true residual is not formed
+__global__ void k_gmres_status(GmresDev G, int j, const int* flags, double* est, double* status)
+{
+    est[0] = fabs(G.g[j + 1]);
+    status[0] = (double)(flags ? flags[0] : 0);
+    status[1] = (double)G.stop[0];
+}
+
+std::atomic<int> g_gmres_lazy_residual{1};
+
+void launch_gmres_status(cudaStream_t s, const GmresDev& G, int j, const int* flags, double* est,
+                         double* status)
+{
+    note_launch();
+    k_gmres_status<<<1, 1, 0, s>>>(G, j, flags, est, status);
+}
+
 void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst,
                    const int* flags, const int* stop, double* status)
 {

@@ -278,6 +278,9 @@ bool launch_mgs_persistent(cudaStream_t s, const double* const* V, double* w, co
 void launch_gmres_givens(cudaStream_t s, const double* part, const GmresDev& G, int j);
 // scal[2] = sqrt(sum part) / bnorm
 // (status != nullptr: also status[0] = flags[0], status[1] = stop[0], as doubles)
+void launch_gmres_status(cudaStream_t s, const GmresDev& G, int j, const int* flags, double* est,
+                         double* status);
+extern std::atomic<int> g_gmres_lazy_residual; // 1: true residual only once the carried estimate nears the tolerance
 void launch_relres(cudaStream_t s, const double* part, const double* bnorm, double* dst,
                    const int* flags = nullptr, const int* stop = nullptr, double* status = nullptr);
 

@@ -1330,16 +1330,37 @@ oc_solve_report Problem::gmres(const oc_ipm_params& p, int kind, const double* b
             }
             launch_gmres_givens(ctx.stream, pa, G, j);
             launch_scale_inv(ctx.stream, kw_.get(), scal + 1, V_[j + 1].get(), n, stop_.get());
-            launch_combine(ctx.stream, Ztab_.get(), yls_.get(), j + 1, x, n,
-                           xbase ? kx2_.get() : nullptr);
-            launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(), x,
-                       nullptr, b, part);
-            // one packed readback per iteration: scalars, error flags, stop code
-            launch_relres(ctx.stream, part, scal + 0, scal + 2, flags_.get(), stop_.get(), scal + 8);
-            launch_check("gmres iteration");
-            cuda_check(cudaMemcpyAsync(ctx.hscal, scal, 10 * sizeof(double), cudaMemcpyDeviceToHost,
-                                       ctx.stream), "readback");
-            ctx.sync();
+            // The reference rebuilds x and forms the true residual every iteration
+            // (krylov.cpp:187-200); neither feeds back into the Krylov iterates, so
+            // they are only formed once the residual norm GMRES carries (|g_{j+1}|,
+            // equal to ||b - A x_j|| up to rounding) is within 1e3 of the tolerance,
+            // and at every exit (cap, restart, exhaustion, zero pivot): same x, same
+            // reported residual, same iteration counts.
+            bool lazy = g_gmres_lazy_residual.load() != 0;
+            if (lazy) {
+                launch_gmres_status(ctx.stream, G, j, flags_.get(), scal + 4, scal + 8);
+                launch_check("gmres iteration");
+                cuda_check(cudaMemcpyAsync(ctx.hscal, scal, 10 * sizeof(double), cudaMemcpyDeviceToHost,
+                                           ctx.stream), "readback");
+                ctx.sync();
+                const double est = ctx.hscal[4] / bnorm;
+                const bool last = total + 1 >= maxit || j + 1 >= restart;
+                lazy = !(est <= 1e3 * p.linear_tol) && !last && !((int)ctx.hscal[9]) &&
+                       !((int)ctx.hscal[8]) && ctx.hscal[1] > 1e-300 && est == est;
+                if (lazy) ctx.hscal[2] = est;
+            }
+            if (!lazy) {
+                launch_combine(ctx.stream, Ztab_.get(), yls_.get(), j + 1, x, n,
+                               xbase ? kx2_.get() : nullptr);
+                launch_kkt(ctx.stream, P, has_sb_ ? ty_.get() : nullptr, tw_.get(), tv_.get(), x,
+                           nullptr, b, part);
+                // one packed readback: scalars, error flags, stop code
+                launch_relres(ctx.stream, part, scal + 0, scal + 2, flags_.get(), stop_.get(), scal + 8);
+                launch_check("gmres iteration");
+                cuda_check(cudaMemcpyAsync(ctx.hscal, scal, 10 * sizeof(double), cudaMemcpyDeviceToHost,
+                                           ctx.stream), "readback");
+                ctx.sync();
+            }
             ctx.hflags[0] = (int)ctx.hscal[8];
             ctx.hflags[1] = (int)ctx.hscal[9];
             check_flags(false);
