@@ -223,7 +223,8 @@ int oc_debug_coarse_op(oc_mg* mg, int pre, int post, double* out);
  * high-priority side stream), "heat_chain" (1: each direction of the heat
  * time-block substitution as one chained cluster launch), "sweep_lean"
  * (variable tiled sweeps: 1 = 1/a_ii, 2 = 1/a_ii and b read in the colour
- * passes instead of staged; default 1),
+ * passes instead of staged, 3 = node records streamed into a shared-memory
+ * ring by a producer warp's bulk copies; default 1),
  * "gmres_lazy_residual" (1: GMRES rebuilds x and forms the true residual only
  * once the residual norm it carries is within 1e3 of the tolerance, and at
  * every exit), "lex_pipeline" (1: the lexicographic sweeps of a smoothing phase run as a

@@ -11,8 +11,8 @@
 // shared memory, so after all passes the tile is exact without inter-CTA
 // synchronisation (redundant halo work). Large variable levels read their
 // coefficients in the passes from a colour-split copy of per-node records
-// (8 off-diagonals = four 16-byte loads from one address; Op9::csplit) with
-// 1/a_ii in the same order, which leaves room for five CTAs per SM.
+// (8 off-diagonals = four 16-byte loads from one address, then 1/a_ii;
+// Op9::csplit), which leaves room for five CTAs per SM.
 // Threads own fixed positions k = t + 256 m of the colour sub-lattice, which
 // are also the shared-memory indices inside a colour plane.
 //
@@ -26,6 +26,10 @@ namespace ocb {
 std::atomic<int> g_sweep_lean{1}; // operands of variable sweeps read in the passes (see SweepShape); 1 measured best (C4 P_T -3%)
 
 namespace {
+
+// words per node record of the colour-split copy: 8 off-diagonals (SW, S, SE, W,
+// E, NW, N, NE), 1/a_ii, one pad word (records stay 16-byte aligned)
+constexpr int kRecW = 10;
 
 __device__ __forceinline__ void cp_async8(void* dst_smem, const void* src)
 {
@@ -102,10 +106,20 @@ struct SweepShape {
     // fit (coalesced row copies, read once per launch for all fused sweeps);
     // otherwise read through L1 (colour-strided, L2-bandwidth bound)
     static constexpr bool CS = VAR && (size_t)11 * RP * sizeof(double) <= 100 * 1024; // >= 2 CTAs/SM
-    static constexpr int LEAN = (VAR && !CS) ? LEAN_ : 0;
+    // LEAN_ = 3 (RING): a producer warp streams each colour pass's node records
+    // (Op9::csplit, one bulk copy per colour row: the TMA engine's 1-D copies,
+    // completion on an mbarrier) into a two-stage ring two passes ahead of the
+    // 256 compute threads, which then read coefficients and 1/a_ii from shared
+    // memory instead of waiting on L2 in every pass.
+    static constexpr bool RING = VAR && !CS && LEAN_ == 3 &&
+                                 ((size_t)2 * RP + 2 * KC * kRecW + (MODE == 2 ? (TX + 1) * (TY + 1) : 0)) * sizeof(double) <=
+                                     112 * 1024; // two CTAs per SM, else the in-pass loads (LEAN 1)
+    static constexpr int LEAN = (VAR && !CS) ? (RING ? 1 : LEAN_) : 0;
     static constexpr int PLANES = CS ? 11 : 3 - LEAN; // x, b, inv (+ 8 off-diagonals)
+    static constexpr int RINGW = RING ? 2 * KC * kRecW : 0; // two stages of KC records
+    static constexpr int THREADS = RING ? 288 : 256;
     static constexpr int RSX = TX + 1, RSN = (TX + 1) * (TY + 1); // MODE 2: fine residual rows
-    static constexpr size_t smem = ((size_t)PLANES * RP + (MODE == 2 ? RSN : 0)) * sizeof(double);
+    static constexpr size_t smem = ((size_t)PLANES * RP + RINGW + (MODE == 2 ? RSN : 0)) * sizeof(double);
     // planar index of region node (lx, ly)
     __host__ __device__ static constexpr int pidx(int lx, int ly)
     {
@@ -131,8 +145,16 @@ struct RestrictOut {
     double* xc;
 };
 
+__device__ __forceinline__ void ring_wait(unsigned bar, unsigned parity)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n RW:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra RW;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
 template <int TX, int TY, int NS, bool VAR, int MODE = 0, int LEAN_ = 0>
-__global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__ b,
+__global__ void __launch_bounds__(SweepShape<TX, TY, NS, VAR, MODE, LEAN_>::THREADS) k_sweep(Op9 A, const double* __restrict__ b,
                                                const double* __restrict__ inv,
                                                const double* __restrict__ xin,
                                                double* __restrict__ xout,
@@ -142,12 +164,22 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     constexpr bool RN = MODE == 1, RR = MODE == 2;
     using S = SweepShape<TX, TY, NS, VAR, MODE, LEAN_>;
     constexpr int H = S::H, RX = S::RX, RY = S::RY, RP = S::RP, PS = S::PS, LEAN = S::LEAN;
+    constexpr bool RING = S::RING;
     constexpr int P = 4 * NS;
     extern __shared__ double sm[];
     double* xs = sm;
     double* bs = xs + RP;
     double* iv = bs + RP;
     double* cs = iv + RP; // VAR: plane p holds entry d = p < 4 ? p : p + 1
+    double* ring = sm + S::PLANES * RP; // RING: two stages of node records
+    __shared__ unsigned long long ring_bar[2];
+    const bool comp = !RING || threadIdx.x < 256; // RING: warp 8 is the producer
+    if (RING && threadIdx.x == 0) {
+        const unsigned b0 = (unsigned)__cvta_generic_to_shared(&ring_bar[0]);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\nmbarrier.init.shared::cta.b64 [%1], 1;\n"
+                     "fence.mbarrier_init.release.cluster;\n" ::"r"(b0), "r"(b0 + 8)
+                     : "memory");
+    }
 
     const int nx = A.nx;
     const long long n = (long long)nx * nx;
@@ -157,7 +189,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 
     // ---- stage the region: every copy in flight before the first wait
-    for (int ly = ty; ly < RY; ly += 8) {
+    for (int ly = comp ? ty : RY; ly < RY; ly += 8) {
         const int gy = oy + ly;
         const bool rowin = gy >= 0 && gy < nx;
         for (int lx = tx; lx < RX; lx += 32) {
@@ -187,7 +219,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     cp_async_wait_all();
     if (ec) {
         __syncthreads();
-        for (int ly = ty; ly < RY; ly += 8) {
+        for (int ly = comp ? ty : RY; ly < RY; ly += 8) {
             const int gy = oy + ly;
             if (gy < 0 || gy >= nx) continue;
             for (int lx = tx; lx < RX; lx += 32) {
@@ -219,6 +251,39 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     long long cpo[9]; // coefficient plane offsets d * n (variable operators)
 #pragma unroll
     for (int d = 0; d < 9; ++d) cpo[d] = (long long)d * n;
+    // RING producer: the records of pass q's colour rows, one bulk copy per row
+    // (lane = colour row), into stage q & 1; bytes complete on that stage's mbarrier
+    auto produce = [&](int q) {
+        const int pc = q & 3;
+        const int c = forward ? pc : 3 - pc;
+        const int cx = c & 1, cy = c >> 1;
+        const int g = P - 1 - q + (RN ? 1 : 0) + (RR ? 2 : 0);
+        const int lox = max(tx0 - g, 0), hix = min(tx0 + TX + g, nx);
+        const int loy = max(ty0 - g, 0), hiy = min(ty0 + TY + g, nx);
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&ring_bar[q & 1]);
+        double* stg = ring + (q & 1) * (S::KC * kRecW);
+        const int lane = threadIdx.x & 31;
+        const int gy = oy + 2 * lane + cy;
+        if (lane < S::CYN && gy >= loy && gy < hiy) {
+            const int k0 = (lox - ox - cx + 1) >> 1;    // first and last colour column in range
+            const int k1 = (hix - 1 - ox - cx) >> 1;
+            if (k1 >= k0) {
+                const unsigned bytes = (unsigned)(k1 - k0 + 1) * kRecW * 8u;
+                const double* src = A.csplit + ((long long)gy * nx + (cx ? ((nx + 1) >> 1) : 0) + (ox >> 1) + k0) * kRecW;
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(stg + (lane * S::CXN + k0) * kRecW);
+                asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                             "l"(src), "r"(bytes), "r"(bar)
+                             : "memory");
+            }
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+    };
+    if (RING && !comp) {
+        produce(0);
+        produce(1);
+    }
 #pragma unroll 1
     for (int q = 0; q < P; ++q) {
         const int pc = q & 3;
@@ -238,6 +303,36 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
             const int sy = dy < 0 ? cy - 1 : (dy > 0 ? cy : 0);
             off[d] = (ncx + 2 * ncy) * PS + sy * CXN + sx;
         }
+        if (RING) {
+            if (comp) {
+                ring_wait((unsigned)__cvta_generic_to_shared(&ring_bar[q & 1]), (unsigned)(q >> 1) & 1u);
+                const double2* stg = reinterpret_cast<const double2*>(ring + (q & 1) * (S::KC * kRecW));
+#pragma unroll
+                for (int m = 0; m < KT; ++m) {
+                    const int gx = kx0[m] + cx, gy = ky0[m] + cy;
+                    if (gx >= lox && gx < hix && gy >= loy && gy < hiy) {
+                        const int k = threadIdx.x + 256 * m;
+                        const int l = lc + k;
+                        const double2* rec = stg + k * (kRecW / 2);
+                        const double2 a01 = rec[0], a23 = rec[1], a45 = rec[2], a67 = rec[3];
+                        const double ivl = rec[4].x;
+                        double s = bs[l];
+                        s -= a01.x * xs[off[0] + k];
+                        s -= a01.y * xs[off[1] + k];
+                        s -= a23.x * xs[off[2] + k];
+                        s -= a23.y * xs[off[3] + k];
+                        s -= a45.x * xs[off[5] + k];
+                        s -= a45.y * xs[off[6] + k];
+                        s -= a67.x * xs[off[7] + k];
+                        s -= a67.y * xs[off[8] + k];
+                        xs[l] = s * ivl;
+                    }
+                }
+            }
+            __syncthreads(); // pass q done: its stage is free
+            if (!comp && q + 2 < P) produce(q + 2);
+            continue;
+        }
 #pragma unroll
         for (int m = 0; m < KT; ++m) {
             const int gx = kx0[m] + cx, gy = ky0[m] + cy;
@@ -250,10 +345,10 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
                 if (VAR && !S::CS && A.csplit) {
                     // the node's record: 8 off-diagonals in four 16-byte loads
                     const int si = ks0[m] + so;
-                    const double2* rec = reinterpret_cast<const double2*>(A.csplit) + (long long)si * 4;
+                    const double2* rec = reinterpret_cast<const double2*>(A.csplit) + (long long)si * (kRecW / 2);
                     const double2 a01 = __ldg(rec), a23 = __ldg(rec + 1), a45 = __ldg(rec + 2),
                                   a67 = __ldg(rec + 3);
-                    const double ivl = LEAN >= 1 ? __ldg(A.isplit + si) : iv[l];
+                    const double ivl = LEAN >= 1 ? __ldg(reinterpret_cast<const double*>(rec + 4)) : iv[l];
                     s -= a01.x * xs[off[0] + k];
                     s -= a01.y * xs[off[1] + k];
                     s -= a23.x * xs[off[2] + k];
@@ -282,7 +377,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     }
 
     double acc = 0.0;
-    for (int ly = ty; ly < TY; ly += 8) {
+    for (int ly = comp ? ty : TY; ly < TY; ly += 8) {
         const int gy = ty0 + ly;
         if (gy >= nx) break;
         for (int lx = tx; lx < TX; lx += 32) {
@@ -313,8 +408,8 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
     if (RR) {
         // fine residual on [tx0, tx0+TX] x [ty0, ty0+TY] (multigrid.cpp:120-121,
         // k_resid_restrict's order), then R = P^T for this tile's coarse nodes
-        double* rs = sm + S::PLANES * RP;
-        for (int ly = ty; ly <= TY; ly += 8) {
+        double* rs = sm + S::PLANES * RP + S::RINGW;
+        for (int ly = comp ? ty : TY + 1; ly <= TY; ly += 8) {
             const int gy = ty0 + ly;
             for (int lx = tx; lx <= TX; lx += 32) {
                 const int gx = tx0 + lx;
@@ -335,7 +430,7 @@ __global__ void __launch_bounds__(256) k_sweep(Op9 A, const double* __restrict__
         }
         __syncthreads();
         const int cx0 = tx0 / 2, cy0 = ty0 / 2;
-        for (int j = ty; j < TY / 2; j += 8) {
+        for (int j = comp ? ty : TY; j < TY / 2; j += 8) {
             const int cy = cy0 + j;
             for (int kx = tx; kx < TX / 2; kx += 32) {
                 const int cx = cx0 + kx;
@@ -456,7 +551,7 @@ __global__ void __launch_bounds__(256) k_resid_restrict(Op9 A, const double* __r
 // loads from one address instead of eight strided planes), and 1/a_ii
 // (k_inv_diag's quotient) in the same node order
 __global__ void k_colour_split(int nx, const double* __restrict__ coef, const double* __restrict__ diag,
-                               double* __restrict__ out, double* __restrict__ iout)
+                               double* __restrict__ out)
 {
     const long long n = (long long)nx * nx;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -465,11 +560,12 @@ __global__ void k_colour_split(int nx, const double* __restrict__ coef, const do
     const long long o = (long long)gy * nx + ((gx & 1) ? ((nx + 1) >> 1) + (gx >> 1) : (gx >> 1));
     const int p = blockIdx.y;
     if (p < 8) {
-        out[o * 8 + p] = coef[(p < 4 ? p : p + 1) * n + i];
+        out[o * kRecW + p] = coef[(p < 4 ? p : p + 1) * n + i];
     } else {
         double a = coef[4 * n + i];
         if (diag) a += diag[i];
-        iout[o] = 1.0 / a;
+        out[o * kRecW + 8] = 1.0 / a;
+        out[o * kRecW + 9] = 0.0;
     }
 }
 
@@ -500,8 +596,8 @@ void sweep_go_lean(cudaStream_t s, const Op9& A, const double* b, const double* 
     (void)attr;
     dim3 grid((A.nx + TX - 1) / TX, (A.nx + TY - 1) / TY);
     note_launch();
-    k_sweep<TX, TY, NS, VAR, MODE, LEAN><<<grid, 256, smem, s>>>(A, b, inv, x, xo, ec, forward ? 1 : 0,
-                                                                  zero_init ? 1 : 0, nc, ro);
+    k_sweep<TX, TY, NS, VAR, MODE, LEAN><<<grid, SweepShape<TX, TY, NS, VAR, MODE, LEAN>::THREADS, smem, s>>>(
+        A, b, inv, x, xo, ec, forward ? 1 : 0, zero_init ? 1 : 0, nc, ro);
 }
 
 template <int TX, int TY, int NS, bool VAR, int MODE>
@@ -511,7 +607,8 @@ void sweep_go_mode(cudaStream_t s, const Op9& A, const double* b, const double* 
 {
     if constexpr (VAR && !SweepShape<TX, TY, NS, VAR, MODE>::CS && NS <= 2) {
         const int lean = g_sweep_lean.load();
-        if (lean == 1) return sweep_go_lean<TX, TY, NS, VAR, MODE, 1>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
+        if (lean == 3 && A.csplit) return sweep_go_lean<TX, TY, NS, VAR, MODE, 3>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
+        if (lean == 1 || lean == 3) return sweep_go_lean<TX, TY, NS, VAR, MODE, 1>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
         if (lean == 2) return sweep_go_lean<TX, TY, NS, VAR, MODE, 2>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
     }
     sweep_go_lean<TX, TY, NS, VAR, MODE, 0>(s, A, b, inv, x, xo, forward, zero_init, ec, nc, ro);
@@ -581,12 +678,11 @@ std::atomic<int> g_colour_split{1};
 std::atomic<int> g_fuse_norm{1};
 std::atomic<int> g_fuse_restrict{1};
 
-void launch_colour_split(cudaStream_t s, int nx, const double* coef, const double* diag, double* out,
-                         double* iout)
+void launch_colour_split(cudaStream_t s, int nx, const double* coef, const double* diag, double* out)
 {
     const long long n = (long long)nx * nx;
     note_launch();
-    k_colour_split<<<dim3((unsigned)((n + 255) / 256), 9), 256, 0, s>>>(nx, coef, diag, out, iout);
+    k_colour_split<<<dim3((unsigned)((n + 255) / 256), 9), 256, 0, s>>>(nx, coef, diag, out);
 }
 
 void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long long fcs,

@@ -60,8 +60,8 @@ void launch_inv_diag(cudaStream_t s, const Op9& A, double* inv, int batch, long 
 extern std::atomic<int> g_mgs_persistent; // GMRES columns j+1 >= this use the persistent MGS launch (0: never)
 extern std::atomic<int> g_sweep_lean;   // variable tiled sweeps: 1 = 1/a_ii, 2 = 1/a_ii and b read in the passes, not staged
 extern std::atomic<int> g_colour_split; // 1: the fine level of >= 1023^2 hierarchies sweeps from it
-void launch_colour_split(cudaStream_t s, int nx, const double* coef, const double* diag, double* out,
-                         double* iout);
+void launch_colour_split(cudaStream_t s, int nx, const double* coef, const double* diag, double* out);
+constexpr int kSplitRecordWords = 10; // words per node of the colour-split copy
 void launch_resid_restrict_tiled(cudaStream_t s, const Op9& A, const double* b, const double* x,
                                  double* bc, double* xc);
 // x += P ec

@@ -22,10 +22,9 @@ struct Op9 {
     double c[9];          // constant stencil (when coef == nullptr)
     const double* diag;   // optional added diagonal (plus_diagonal), or nullptr
     double cscale;        // constant stencil multiplier (1 unless stated)
-    const double* csplit; // optional colour-split copy of the 8 off-diagonals read by the
-                          // tiled sweep: node records of 8 words (SW,S,SE,W,E,NW,N,NE),
+    const double* csplit; // optional colour-split copy read by the tiled sweep: node
+                          // records of 10 words (SW,S,SE,W,E,NW,N,NE, 1/a_ii, pad),
                           // row y holding its even-x nodes first, then its odd-x nodes
-    const double* isplit; // 1/a_ii in the same node order (set with csplit)
 };
 
 constexpr int kRedBlocks = 296;   // fixed reduction grid: 2 x 148 SMs (deterministic)

@@ -268,7 +268,6 @@ Op9 Hierarchy::level_op(int k, int bt) const
         if (a.coef) a.coef += bt * fine_coef_stride_;
         if (a.diag) a.diag += bt * fine_diag_stride_;
         a.csplit = bt == 0 && split_.size() > 0 && split_[0] ? split_[0].get() : nullptr;
-        a.isplit = a.csplit ? isplit_[0].get() : nullptr;
         return a;
     }
     Op9 a{};
@@ -277,7 +276,6 @@ Op9 Hierarchy::level_op(int k, int bt) const
     a.diag = nullptr;
     a.cscale = 1.0;
     a.csplit = bt == 0 && (size_t)k < split_.size() && split_[k] ? split_[k].get() : nullptr;
-    a.isplit = a.csplit ? isplit_[k].get() : nullptr;
     return a;
 }
 
@@ -329,20 +327,15 @@ void Hierarchy::build_split(Ctx& c)
     if (split_.size() != (size_t)K_ + 1) {
         split_.clear();
         split_.resize(K_ + 1);
-        isplit_.clear();
-        isplit_.resize(K_ + 1);
     }
     for (int k = 0; k <= K_; ++k) {
         const double* src = k == 0 ? fine_.coef : coef_[k].get();
         const double* before = split_[k].get();
         if (!on || k >= kb_ || !src || nx_[k] < 500) {
             split_[k].release();
-            isplit_[k].release();
         } else {
-            split_[k].resize(8 * (size_t)level_n(k));
-            isplit_[k].resize((size_t)level_n(k));
-            launch_colour_split(c.stream, nx_[k], src, k == 0 ? fine_.diag : nullptr, split_[k].get(),
-                                isplit_[k].get());
+            split_[k].resize((size_t)kSplitRecordWords * level_n(k));
+            launch_colour_split(c.stream, nx_[k], src, k == 0 ? fine_.diag : nullptr, split_[k].get());
         }
         if (split_[k].get() != before) ++gen_; // captured graphs hold the old pointers
     }

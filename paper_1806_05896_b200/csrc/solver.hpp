@@ -215,7 +215,6 @@ private:
     DVec lu_;
     DevArray<int> perm_;
     std::vector<DVec> split_;       // [k] colour-split off-diagonal records of variable tiled levels >= 511^2 (batch 1)
-    std::vector<DVec> isplit_;      // [k] 1/a_ii in the same node order
     DVec cop_;                      // cluster: batch x 225 x 225 dense levels <= 4 cycle operator
     int cop_pre_ = -1, cop_post_ = -1; // sweep counts cop_ was computed for (-1: stale)
     DVec part_, state_;

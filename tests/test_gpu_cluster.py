@@ -256,11 +256,11 @@ def test_tiled_heat_kkt_apply_equals_per_node_kernel(oc, ctx, lib):
     assert np.array_equal(out[0], out[1])
 
 
-@pytest.mark.parametrize("lean", [0, 2])
-def test_lean_variable_sweeps_bitwise_equal(oc, ctx, lib, lean):
-    """Variable-coefficient tiled sweeps that read 1/a_ii (and b) in the colour
-    passes instead of staging them (sweep_lean) reproduce the default bits."""
-    ell = 9
+@pytest.mark.parametrize("lean,ell", [(0, 9), (2, 9), (3, 9), (3, 10)])
+def test_lean_variable_sweeps_bitwise_equal(oc, ctx, lib, lean, ell):
+    """Variable-coefficient tiled sweeps that stage 1/a_ii (0), read b in the
+    colour passes too (2), or take their node records from a shared-memory ring
+    filled by a producer warp's bulk copies (3) reproduce the default bits."""
     L = oc.assemble9("convdiff", ell, eps=0.02)
     L[4] += 1.0
     b = np.random.default_rng(11).uniform(-1, 1, L.shape[1])
