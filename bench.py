@@ -502,7 +502,11 @@ def run_ours_c5(args, torch, dist, rank, world, local):
     torch.cuda.synchronize()
     for cx in ctxs:
         cx.profile(True)
+    t_prof = time.perf_counter()
     replicas.run_concurrent(solve, range(R))
+    for cx in ctxs:
+        cx.synchronize()
+    t_prof = (time.perf_counter() - t_prof) * 1e3
     blk_ms, blk_n = 0.0, 0
     for cx in ctxs:
         pr = cx.profile_read()
@@ -568,6 +572,11 @@ def run_ours_c5(args, torch, dist, rank, world, local):
             "peak_source": peak_src, "bytes_per_launch": blk_bytes,
             "avg_launch_ms": blk_ms / blk_n if blk_n else None, "launches_in_pass": blk_n,
             "block_solves_per_launch": per_launch,
+            "in_flight": {"avg_concurrent_launches": blk_ms / t_prof if t_prof else None,
+                          "aggregate_achieved": blk_n * blk_bytes / (t_prof / 1e3) / 1e9 if t_prof else None,
+                          "aggregate_frac": blk_n * blk_bytes / (t_prof / 1e3) / 1e9 / peak if t_prof else None,
+                          "note": f"the same kernel's launches of all {R} solves over that untimed step's "
+                                  "wall time (at most 7 of these 16-CTA clusters are resident)"},
             "avg_block_solve_ms": blk_ms / blk_n / per_launch if blk_n else None,
             "note": "achieved = SURVEY 8d algorithmic bytes of the launch's block MG solves (287 "
                     "words per node each) / its CUDA-event time on the solver streams in an "
