@@ -537,6 +537,7 @@ def run_ours_c5(args, torch, dist, rank, world, local):
     # iteration plus the P_D apply that starts each Newton solve) over the steps' device time
     n_applies = sum(r.total_lin + r.stats.nli for res in results for r in res)
     agg_gbs = n_applies * (kkt_b + prec_b) / (max_ms / 1e3) / 1e9  # this rank's GPU
+    n_chain = n_applies * (2 if per_launch > 1 else 2 * c.nt)  # launches of the block kernel in the timed steps
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -572,11 +573,13 @@ def run_ours_c5(args, torch, dist, rank, world, local):
             "peak_source": peak_src, "bytes_per_launch": blk_bytes,
             "avg_launch_ms": blk_ms / blk_n if blk_n else None, "launches_in_pass": blk_n,
             "block_solves_per_launch": per_launch,
-            "in_flight": {"avg_concurrent_launches": blk_ms / t_prof if t_prof else None,
-                          "aggregate_achieved": blk_n * blk_bytes / (t_prof / 1e3) / 1e9 if t_prof else None,
-                          "aggregate_frac": blk_n * blk_bytes / (t_prof / 1e3) / 1e9 / peak if t_prof else None,
-                          "note": f"the same kernel's launches of all {R} solves over that untimed step's "
-                                  "wall time (at most 7 of these 16-CTA clusters are resident)"},
+            "in_flight": {"launches_in_timed_steps": n_chain,
+                          "avg_concurrent_launches": (n_chain * blk_ms / blk_n / max_ms) if blk_n else None,
+                          "aggregate_achieved": n_chain * blk_bytes / (max_ms / 1e3) / 1e9,
+                          "aggregate_frac": n_chain * blk_bytes / (max_ms / 1e3) / 1e9 / peak,
+                          "note": f"the same kernel's launches of all {R} solves in the timed steps "
+                                  "(substitution directions x P_D applies) over the steps' device time; at "
+                                  "most 7 of these 16-CTA clusters are resident"},
             "avg_block_solve_ms": blk_ms / blk_n / per_launch if blk_n else None,
             "note": "achieved = SURVEY 8d algorithmic bytes of the launch's block MG solves (287 "
                     "words per node each) / its CUDA-event time on the solver streams in an "
