@@ -1185,8 +1185,9 @@ void Problem::precond_apply_direct(int kind, const double* r, double* out)
     // BlockDiagPrecond (precond.cpp:202-212) / BlockTriPrecond (:214-230)
     ChebWork w{cg_.get(), c0_.get(), c1_.get(), c2_.get()};
     if (heat_ && kind == OC_PRECOND_PD && g_heat_fork.load()) {
-        // P_D's three blocks are independent: the time-block substitution (256
-        // dependent cluster launches) runs on the high-priority side stream
+        // P_D's three blocks are independent: the time-block substitution (two
+        // chained cluster launches, 256 dependent block solves) runs on the
+        // high-priority side stream
         // while Chebyshev and the 2x2 blocks run here; with several solves in
         // flight the priority lets the cluster launches claim their SMs ahead
         // of other solves' wide kernels
